@@ -1,0 +1,329 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 IB time step (BASELINE.json metric: IB time steps/s at 256^3, fp64).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+
+One "step" = one full IB time step (force, spread, fluid solve, interpolate, update) of
+BASELINE.json configs[3] (256^3 grid, 2,097,152 Lagrangian points), synthetic seeded
+inputs (gen/).  N > 1: one process per GPU (torchrun), each running an independent
+replica (DESIGN.md §7 "replicas only"; no data-path collective), timed on the device and
+reduced as the max over ranks; value = total steps of all ranks / time.
+`--impl reference` times the CPU oracle (the reference arm of this tier) on the host.
+Prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "IB time steps/sec at 256^3 grid (fp64); per-stage achieved HBM GB/s vs peak"
+UNIT = "steps/s"
+
+
+# ------------------------------------------------------------------ algorithmic bytes
+def stage_bytes(N: int, np_: int, nd: int = 0) -> dict:
+    """Compulsory HBM bytes per launch of each stage (DESIGN.md §6 byte model).
+    V = N^3 cells, C = N^2 (N/2+1) complex modes per component."""
+    V = N ** 3
+    C = N * N * (N // 2 + 1)
+    return {
+        # X (24) + neighbour X (24, cached) + per-point k/L0 (32) -> 80 B/pt; F band RMW
+        # is on-chip (L2 atomics) and not counted
+        "force_spread": 80 * np_,
+        "xfwd_rhs_r2c": 24 * V + 24 * V + 48 * C,     # read u, read F, write r^ (x-spectrum)
+        "y_fwd": 96 * C,                              # read + write 3 complex components
+        "z_solve": 96 * C,
+        "y_inv": 96 * C,
+        "xinv_c2r": 48 * C + 24 * V,                  # read spectrum, write u^{n+1}
+        "interp_update": 48 * np_,                    # read X, write X (u band from L2)
+    }
+
+
+def load_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(stage: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch for `stage` from the committed
+    ncu --set full summary (profiles/ncu_traffic.json), else None."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        d = json.load(open(p))
+        v = d.get("stages", {}).get(stage)
+        return None if v is None else float(v)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=6)
+
+    def summary(self) -> dict:
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in self.rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(self.rows)}
+
+
+# ------------------------------------------------------------------ distributed helpers
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def reduce_max(x: float) -> float:
+    """Max over ranks (the timed region's duration); identity without a process group."""
+    import torch
+    import torch.distributed as dist
+    if not (dist.is_available() and dist.is_initialized()):
+        return float(x)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([float(x)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier():
+    import torch.distributed as dist
+    if dist.is_available() and dist.is_initialized():
+        dist.barrier()
+
+
+# ------------------------------------------------------------------ reference arm (oracle)
+def run_reference(args, ws, rank):
+    if rank != 0:
+        return 0
+    import oracle
+    from gen import make_config
+    oracle.set_threads(os.cpu_count() or 1)
+    cfg = make_config(args.config)
+    o = oracle.Oracle.from_config(cfg)
+    k = max(1, min(args.steps, args.ref_max_steps))
+    w = min(args.warmup, 1)
+    o.step(w)
+    t0 = time.perf_counter()
+    o.step(k)
+    dt = time.perf_counter() - t0
+    v = k / dt
+    sample = f"{k} full IB steps of cfg{args.config} ({cfg.N}^3, {cfg.np_} points) after {w} warm-up"
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": ws,
+            "steps": k, "warmup": w, "ms_per_step": 1e3 * dt / k, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg, args.config),
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.get_threads(),
+                             "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def workload_config(cfg, k):
+    return {"workload": f"BASELINE.json configs[{k - 1}] ({cfg.name}): {cfg.N}^3 periodic grid, "
+                        f"{cfg.np_} Lagrangian points",
+            "N": cfg.N, "lagrangian_points": cfg.np_, "global_batch": 1,
+            "parallelism": "replicas", "l2": "inputs larger than L2 (u + spectrum >> 126 MB)"
+            if cfg.N >= 256 else "working set fits in L2 (no flush)"}
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, ws, rank, local):
+    import torch
+    from gen import make_config
+    from paper_math_0301321_b200 import IBContext, IB_OPT_STAGE_TIMING
+    from paper_math_0301321_b200 import ib as ibmod
+
+    torch.cuda.set_device(local)
+    cfg = make_config(args.config)
+    N, npts = cfg.N, cfg.np_
+    ctx = IBContext.from_config(cfg)
+    stream = torch.cuda.Stream()
+    ctx.set_stream(stream.cuda_stream)
+    with torch.cuda.stream(stream):
+        ctx.step(args.warmup)                              # untimed warm-up
+        ctx.set_option(IB_OPT_STAGE_TIMING, 1)
+        ctx.stage_times(reset=True)
+        ctx.launch_count(reset=True)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            ctx.step(args.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        launches = ctx.launch_count(reset=True)
+        stages = ctx.stage_times(reset=True)
+        ctx.set_option(IB_OPT_STAGE_TIMING, 0)
+    ms_max = reduce_max(ms)
+    value = ws * args.steps / (ms_max / 1e3)
+
+    # per-stage roofline against the measured HBM copy peak
+    peaks = load_peaks()
+    sb = stage_bytes(N, npts)
+    per_stage = {}
+    for k, t in stages.items():
+        avg = t / args.steps
+        gbs = sb[k] / (avg / 1e3) / 1e9 if avg > 0 else None
+        per_stage[k] = {"ms": avg, "alg_bytes": sb[k], "gbs": gbs,
+                        "frac": gbs / peaks["hbm_gbs"] if gbs else None}
+    dom = max(stages, key=lambda k: stages[k])
+    avg_dom = stages[dom] / args.steps
+    achieved = sb[dom] / (avg_dom / 1e3) / 1e9
+    step_bytes = sum(sb.values())
+    roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
+            "peak_source": peaks["source"],
+            "step": {"alg_bytes": step_bytes, "ms": ms_max / args.steps,
+                     "gbs": step_bytes / (ms_max / args.steps / 1e3) / 1e9,
+                     "frac": step_bytes / (ms_max / args.steps / 1e3) / 1e9 / peaks["hbm_gbs"],
+                     "frac_of_nominal_8tbs": step_bytes / (ms_max / args.steps / 1e3) / 8e12}}
+
+    # end-to-end through the C-ABI with pinned host buffers: per step H2D (u, X), step,
+    # D2H (u, X)
+    ke = max(2, min(args.steps, args.e2e_steps))
+    hu = torch.empty((3, N, N, N), dtype=torch.float64).pin_memory()
+    hX = torch.empty((npts, 3), dtype=torch.float64).pin_memory()
+    ctx.get_fields_into(hu)
+    ctx.get_positions_into(hX)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(ke):
+        ibmod.ib_set_velocity(ctx.ctx, hu, N)
+        ibmod.ib_set_positions(ctx.ctx, hX)
+        ctx.step(1)
+        ctx.get_fields_into(hu)
+        ctx.get_positions_into(hX)
+    torch.cuda.synchronize()
+    te = reduce_max(time.perf_counter() - t0)
+    e2e = {"value": ws * ke / te, "unit": UNIT, "h2d_bytes_per_step": hu.numel() * 8 + hX.numel() * 8,
+           "d2h_bytes_per_step": hu.numel() * 8 + hX.numel() * 8, "steps": ke,
+           "path": "ib_set_velocity + ib_set_positions (pinned host) -> ib_step(1) -> "
+                   "ib_get_fields + ib_get_positions (pinned host)"}
+    ctx.close()
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(args)
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f64", "data": "synthetic", "config": workload_config(cfg, args.config),
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+                "gpu_launches": launches,
+                "throughput": {"cells_per_s": value * N ** 3, "points_per_s": value * npts},
+                "stages": per_stage}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+def cpu_baseline(args):
+    """The oracle as it stands, on this host's cores, on a bounded sample: 1 IB step of
+    the same config (about 10 s at 256^3 on 8 cores)."""
+    import oracle
+    from gen import make_config
+    oracle.set_threads(os.cpu_count() or 1)
+    cfg = make_config(args.config)
+    o = oracle.Oracle.from_config(cfg)
+    t0 = time.perf_counter()
+    o.step(1)
+    dt = time.perf_counter() - t0
+    return {"value": 1.0 / dt, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+            "sample": f"1 full IB step of cfg{args.config} ({cfg.N}^3, {cfg.np_} points)"}
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--ref-max-steps", type=int, default=6)
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3                                    # timing rule: W >= 3
+    ws, rank, local = dist_env()
+    if args.impl == "reference":
+        return run_reference(args, ws, rank)      # rank 0 only; no process group needed
+    if ws > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    try:
+        return run_ours(args, ws, rank, local)
+    finally:
+        if ws > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,139 @@
+/* ib.h — C-ABI of the B200 (sm_100a) immersed-boundary time step.
+ *
+ * The operation served is the first-order IB time step of PAPER.md §3.2 (lines 592-761):
+ * given (u^n, X^n) produce (u^{n+1}, X^{n+1}) by
+ *   1. the nodal Lagrangian force f^n                          (PAPER.md 610-616)
+ *   2. spreading F^n = sum_q f^n(q) delta_h(x - X^n(q))          (eq:discreteF, 712-723)
+ *   3. the upwind / implicit-viscosity Navier-Stokes system solved by FFT
+ *                                                                (eq:discreteNS1-2, 659-695)
+ *   4. X^{n+1} = X^n + dt sum_x u^{n+1}(x) delta_h(x - X^n) h^3  (eq:discreteX, 725-734)
+ * with Peskin's 4-point delta_h (745-759) on a periodic N^3 lattice x = h(i,j,k).
+ *
+ * Conventions (all calls):
+ *  - every floating-point array is fp64;
+ *  - every pointer argument may be HOST or DEVICE memory (CUDA unified addressing decides);
+ *    the library copies in/out synchronously on the context's stream and keeps no
+ *    reference to caller memory after the call returns; the caller owns all its buffers;
+ *  - fields are SoA [3][N][N][N] = [component][z][y][x], x fastest; p is [N][N][N];
+ *  - positions and nodal forces are AoS [np][3]; positions are unwrapped (indices mod N);
+ *  - one ctx = one state = one CUDA stream; calls on one ctx must be externally
+ *    serialised; the library owns all device memory of a ctx;
+ *  - return codes: IB_OK (0) or a negative IB_E*; ib_last_error() gives a thread-local
+ *    message for the last failing call.
+ */
+#ifndef IB_B200_H
+#define IB_B200_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ib_ctx ib_ctx;
+
+enum {
+  IB_OK = 0,
+  IB_EINVAL = -1,       /* bad argument (shape, range, NULL, non-finite input)            */
+  IB_ENOMEM = -2,       /* device allocation failed                                       */
+  IB_ECUDA = -3,        /* CUDA runtime error (message in ib_last_error)                  */
+  IB_ENONFINITE = -4,   /* a non-finite u or X appeared during ib_step                     */
+  IB_ESTATE = -5,       /* call not valid in the current state (e.g. no structure set)    */
+  IB_EDEGENERATE = -6   /* a link of zero length at rest                                 */
+};
+
+/* Patch flags: link families present in a structured patch (PAPER.md Q lattice, 697-710). */
+enum {
+  IB_WRAP1 = 1, IB_WRAP2 = 2,              /* i1 / i2 direction periodic                  */
+  IB_STRETCH1 = 4, IB_STRETCH2 = 8,        /* (i1,i2)-(i1+1,i2) and (i1,i2)-(i1,i2+1)      */
+  IB_BEND1 = 16, IB_BEND2 = 32,            /* (i1,i2)-(i1+2,i2) and (i1,i2)-(i1,i2+2)      */
+  IB_TETHER = 64                           /* point tied to an anchor Y with stiffness kt */
+};
+
+/* One structured Lagrangian patch.  Point (i1,i2) is global index first + i2*n1 + i1.
+ * Its block in stiffness[] starts at param_off (in doubles) and holds, in this order:
+ * for each link family present (STRETCH1, STRETCH2, BEND1, BEND2): k[n1*n2] then
+ * L0[n1*n2], indexed by the link's lower-index endpoint (i1,i2); for IB_TETHER:
+ * kt[n1*n2] then Y[n1*n2*3].  A spring adds k(|d| - L0) d/|d| (d = X_j - X_i) to point i,
+ * a tether adds kt (Y_i - X_i).  Forces are nodal (f * dq folded in; spread uses them as
+ * F = sum F_node delta_h, reading Z12). */
+typedef struct {
+  int64_t first;
+  int32_t n1, n2;
+  uint32_t flags;
+  uint32_t pad_;          /* must be 0 */
+  int64_t param_off;
+} ib_patch;
+
+/* Options for ib_set_option. */
+enum {
+  IB_OPT_PRESSURE = 1,      /* 1: the last step of every ib_step batch also produces p   */
+  IB_OPT_STAGE_TIMING = 2,  /* 1: record per-stage CUDA events inside ib_step            */
+  IB_OPT_GRAPH = 3          /* 1 (default): run steps as a captured CUDA graph           */
+};
+
+/* Create a context for an N^3 periodic lattice of mesh width h (domain [0, N h)^3), fluid
+ * density rho, viscosity mu, time step dt (PAPER.md 519-523, 602-605, 632-633).
+ * Rejects: N not a power of two or N < 8 or N > 512; h <= 0; rho <= 0; mu < 0; dt <= 0.
+ * The fluid starts at rest, no structure, step counter n = 0.  NULL on error. */
+ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt);
+void ib_destroy(ib_ctx *ctx);
+
+/* Run all work of ctx on this CUDA stream (a cudaStream_t, e.g. torch's current stream);
+ * NULL selects the library's own stream. */
+int ib_set_stream(ib_ctx *ctx, void *cuda_stream);
+int ib_set_option(ib_ctx *ctx, int32_t option, int64_t value);
+
+/* Lagrangian structure: np points [np][3]; npatch patches covering points [0, np) with
+ * stiffness[nstiff] as described above.  Rejects non-finite or out-of-range data and
+ * (IB_EDEGENERATE) a link whose endpoints coincide at the given positions. */
+int ib_set_structure(ib_ctx *ctx, const double *points, int64_t np, const ib_patch *patches,
+                     int32_t npatch, const double *stiffness, int64_t nstiff);
+/* Replace positions only ([np][3], same np as the structure). */
+int ib_set_positions(ib_ctx *ctx, const double *points);
+/* Fluid velocity u^n, [3][N][N][N]. */
+int ib_set_velocity(ib_ctx *ctx, const double *u);
+/* External drive (PAPER.md 988-993, simplified): F_idx[d] += amp * sin(2 pi n / period) *
+ * dir[d] at step n (t^n = n dt).  n = 0 clears the drive. */
+int ib_set_drive(ib_ctx *ctx, const int64_t *idx, int64_t n, const double *dir,
+                 double amp_per_point, int32_t period_steps);
+
+/* Advance nsteps time steps; synchronises the stream at the end.  Returns IB_ENONFINITE
+ * (ib_last_error names the step) if u or X became non-finite. */
+int ib_step(ib_ctx *ctx, int32_t nsteps);
+
+/* Copy out u^n ([3][N^3], may be NULL) and p^n ([N^3], may be NULL; needs
+ * IB_OPT_PRESSURE enabled before the last ib_step, else IB_ESTATE). */
+int ib_get_fields(ib_ctx *ctx, double *u, double *p);
+int ib_get_positions(ib_ctx *ctx, double *X);
+int64_t ib_get_step(ib_ctx *ctx);
+int ib_set_step(ib_ctx *ctx, int64_t n);
+int64_t ib_num_points(ib_ctx *ctx);
+
+/* Per-stage device time (ms) accumulated since the last reset while IB_OPT_STAGE_TIMING
+ * is on.  names: NUL-separated stage names written to names_buf (may be NULL).  Returns
+ * the number of stages (<= cap). reset != 0 zeroes the accumulators afterwards. */
+int ib_stage_times(ib_ctx *ctx, double *ms, int32_t cap, char *names_buf, int32_t names_cap,
+                   int32_t reset);
+/* Number of library kernel launches issued since the last reset (reset != 0 zeroes). */
+int64_t ib_launch_count(ib_ctx *ctx, int32_t reset);
+
+const char *ib_last_error(void);
+
+/* ---- test-only entry points (same library; not part of the product contract) ----------
+ * Each runs ONE stage of the step on the given inputs with the same kernels ib_step uses. */
+int ib_debug_force(ib_ctx *ctx, double *f_out);                         /* [np][3], step n  */
+int ib_debug_spread(ib_ctx *ctx, const double *f_node, double *F_out);   /* [np][3]->[3][V]  */
+int ib_debug_interp(ib_ctx *ctx, const double *u, double *U_out);        /* [3][V]->[np][3]  */
+/* r = rho u/dt - rho sum_k u_k D_k^{+-} u + F  ([3][V] each) */
+int ib_debug_rhs(ib_ctx *ctx, const double *u, const double *F, double *r_out);
+/* u^{n+1}, p^{n+1} from (u^n, F^n): the fluid part of the step (p_out may be NULL). */
+int ib_debug_fluid(ib_ctx *ctx, const double *u, const double *F, double *u_out,
+                   double *p_out);
+/* Forward 3-D real-to-complex DFT of a real field [N^3] (unnormalised, e^{-2 pi i k.j/N}):
+ * out = complex half spectrum [N][N][N/2+1] as interleaved (re, im). */
+int ib_debug_fft(ib_ctx *ctx, const double *in, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

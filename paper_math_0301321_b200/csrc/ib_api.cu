@@ -1,0 +1,552 @@
+// ib_api.cu — the C-ABI of include/ib.h: context, validation, memory, the step loop.
+//
+// One ib_step step is 6-8 launches on the context stream:
+//   force+spread [+drive spread] -> xfwd (rhs + R2C-x) -> y fwd -> z fwd+solve+inv
+//   -> y inv -> xinv (C2R-x, u^{n+1}) -> interp+update (X^{n+1}).
+// Steps are optionally captured once as a CUDA graph and replayed (IB_OPT_GRAPH); the
+// step index then lives in device memory (incremented by the xfwd kernel).
+#include <cuda_runtime.h>
+
+#include <climits>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "ib_internal.cuh"
+
+using namespace ibk;
+
+static thread_local std::string g_err;
+
+static int fail(int code, const std::string &msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(expr)                                                                    \
+  do {                                                                              \
+    cudaError_t e_ = (expr);                                                        \
+    if (e_ != cudaSuccess)                                                          \
+      return fail(e_ == cudaErrorMemoryAllocation ? IB_ENOMEM : IB_ECUDA,           \
+                  std::string(#expr) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+
+namespace {
+
+template <class T>
+cudaError_t dalloc(T **p, size_t count) {
+  return cudaMalloc((void **)p, count * sizeof(T) > 0 ? count * sizeof(T) : 1);
+}
+
+void dfree(void *p) {
+  if (p) cudaFree(p);
+}
+
+// Copy count elements from a host-or-device pointer to a host vector.
+template <class T>
+cudaError_t to_host(std::vector<T> &dst, const T *src, size_t count, cudaStream_t s) {
+  dst.resize(count);
+  if (!count) return cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(dst.data(), src, count * sizeof(T), cudaMemcpyDefault, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+cudaError_t copy_sync(void *dst, const void *src, size_t bytes, cudaStream_t s) {
+  if (!bytes) return cudaSuccess;
+  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(s);
+}
+
+__global__ void k_count_nonfinite(const double *a, size_t n, unsigned long long *cnt) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
+  unsigned long long c = 0;
+  for (; i < n; i += stride) c += !isfinite(a[i]);
+  if (c) atomicAdd(cnt, c);
+}
+
+__global__ void k_set_ll(long long *p, long long v) { *p = v; }
+
+int count_nonfinite(ib_ctx *c, const double *d, size_t n, unsigned long long *out) {
+  unsigned long long *cnt;
+  CK(cudaMalloc(&cnt, sizeof(*cnt)));
+  cudaMemsetAsync(cnt, 0, sizeof(*cnt), c->stream);
+  k_count_nonfinite<<<592, 256, 0, c->stream>>>(d, n, cnt);
+  c->launches++;
+  cudaError_t e = cudaMemcpyAsync(out, cnt, sizeof(*cnt), cudaMemcpyDeviceToHost, c->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(c->stream);
+  cudaFree(cnt);
+  CK(e);
+  return IB_OK;
+}
+
+StructDev struct_dev(const ib_ctx *c) {
+  StructDev s;
+  s.X = c->X; s.np = c->np; s.patches = c->patches; s.npatch = c->npatch; s.stiff = c->stiff;
+  s.nd = c->nd; s.drive_idx = c->drive_idx; s.drive_dir = c->drive_dir;
+  s.drive_amp = c->drive_amp; s.drive_period = c->drive_period;
+  return s;
+}
+
+void free_graph(ib_ctx *c) {
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  c->graph = nullptr;
+  c->graph_key = -1;
+}
+
+// Enqueue one step.  dev_n != null: step index read from device memory (graph replay).
+cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long long n,
+                         cudaEvent_t *ev) {
+  const FluidGeom &g = c->g;
+  cudaStream_t s = c->stream;
+  StructDev sd = struct_dev(c);
+  cudaError_t e;
+  auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], s); };
+  mark(0);
+  if ((e = launch_force_spread(sd, g, nullptr, dev_n, n, c->F, s)) != cudaSuccess) return e;
+  mark(1);
+  if ((e = launch_xfwd(g, 0, c->u, c->F, nullptr, nullptr, c->spec, 3, c->twN, c->twM, s)) != cudaSuccess) return e;
+  mark(2);
+  if ((e = launch_ypass(g, -1, c->spec, 3, c->twN, s)) != cudaSuccess) return e;
+  mark(3);
+  if ((e = launch_zpass(g, 0, c->spec, pressure ? c->pspec : nullptr, c->twN, c->sym_s,
+                        c->sym_l, s)) != cudaSuccess) return e;
+  mark(4);
+  if ((e = launch_ypass(g, +1, c->spec, 3, c->twN, s)) != cudaSuccess) return e;
+  mark(5);
+  if ((e = launch_xinv(g, c->spec, c->u, 3, c->twN, c->twM, c->flag, dev_n, n, s)) != cudaSuccess) return e;
+  mark(6);
+  if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, s)) != cudaSuccess) return e;
+  mark(7);
+  return cudaSuccess;
+}
+
+int64_t launches_per_step(const ib_ctx *c) {
+  return 5 + (c->np > 0 ? 2 : 0) + (c->nd > 0 && c->np >= 0 ? 1 : 0);
+}
+
+struct Tmp {
+  std::vector<void *> ptrs;
+  ~Tmp() { for (void *p : ptrs) cudaFree(p); }
+  template <class T> cudaError_t get(T **p, size_t n) {
+    cudaError_t e = dalloc(p, n);
+    if (e == cudaSuccess) ptrs.push_back(*p);
+    return e;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+const char *ib_last_error(void) { return g_err.c_str(); }
+
+ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
+  if (N < 8 || N > 512 || (N & (N - 1))) { fail(IB_EINVAL, "N must be a power of two in [8, 512]"); return nullptr; }
+  if (!(h > 0) || !std::isfinite(h)) { fail(IB_EINVAL, "h must be > 0"); return nullptr; }
+  if (!(rho > 0) || !std::isfinite(rho)) { fail(IB_EINVAL, "rho must be > 0"); return nullptr; }
+  if (!(mu >= 0) || !std::isfinite(mu)) { fail(IB_EINVAL, "mu must be >= 0"); return nullptr; }
+  if (!(dt > 0) || !std::isfinite(dt)) { fail(IB_EINVAL, "dt must be > 0"); return nullptr; }
+  ib_ctx *c = new ib_ctx();
+  c->g.N = N; c->g.M = N / 2; c->g.P = N / 2 + 2;
+  c->g.V = (int64_t)N * N * N;
+  c->g.h = h; c->g.invh = 1.0 / h; c->g.rho = rho; c->g.mu = mu; c->g.dt = dt;
+  auto bad = [&](cudaError_t e, const char *what) {
+    fail(e == cudaErrorMemoryAllocation ? IB_ENOMEM : IB_ECUDA,
+         std::string("ib_create: ") + what + ": " + cudaGetErrorString(e));
+    ib_destroy(c);
+    return (ib_ctx *)nullptr;
+  };
+  cudaError_t e;
+  if ((e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking)) != cudaSuccess) return bad(e, "stream");
+  c->stream = c->own_stream;
+  const size_t V = (size_t)c->g.V;
+  const size_t S = (size_t)3 * N * N * c->g.P;
+  if ((e = dalloc(&c->u, 3 * V)) != cudaSuccess) return bad(e, "u");
+  if ((e = dalloc(&c->F, 3 * V)) != cudaSuccess) return bad(e, "F");
+  if ((e = dalloc(&c->spec, S)) != cudaSuccess) return bad(e, "spectrum");
+  if ((e = dalloc(&c->twN, N)) != cudaSuccess) return bad(e, "tables");
+  if ((e = dalloc(&c->twM, N / 2)) != cudaSuccess) return bad(e, "tables");
+  if ((e = dalloc(&c->sym_s, N)) != cudaSuccess) return bad(e, "tables");
+  if ((e = dalloc(&c->sym_l, N)) != cudaSuccess) return bad(e, "tables");
+  if ((e = dalloc(&c->flag, 1)) != cudaSuccess) return bad(e, "flag");
+  if ((e = dalloc(&c->dev_n, 1)) != cudaSuccess) return bad(e, "flag");
+  if ((e = cudaMallocHost(&c->flag_h, sizeof(long long))) != cudaSuccess) return bad(e, "flag");
+  for (int k = 0; k <= STAGE_COUNT; ++k)
+    if ((e = cudaEventCreate(&c->ev[k])) != cudaSuccess) return bad(e, "events");
+  if ((e = cudaMemsetAsync(c->u, 0, 3 * V * sizeof(double), c->stream)) != cudaSuccess) return bad(e, "memset");
+  if ((e = cudaMemsetAsync(c->F, 0, 3 * V * sizeof(double), c->stream)) != cudaSuccess) return bad(e, "memset");
+  if ((e = fluid_setup_attributes(N)) != cudaSuccess) return bad(e, "attributes");
+  if ((e = init_tables(c)) != cudaSuccess) return bad(e, "tables");
+  if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return bad(e, "sync");
+  return c;
+}
+
+void ib_destroy(ib_ctx *c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  free_graph(c);
+  dfree(c->u); dfree(c->F); dfree(c->spec); dfree(c->pspec); dfree(c->p);
+  dfree(c->twN); dfree(c->twM); dfree(c->sym_s); dfree(c->sym_l);
+  dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->drive_idx); dfree(c->drive_dir);
+  dfree(c->flag); dfree(c->dev_n);
+  if (c->flag_h) cudaFreeHost(c->flag_h);
+  for (int k = 0; k <= STAGE_COUNT; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
+  for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+  if (c->own_stream) cudaStreamDestroy(c->own_stream);
+  delete c;
+}
+
+int ib_set_stream(ib_ctx *c, void *stream) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  CK(cudaStreamSynchronize(c->stream));
+  c->stream = stream ? (cudaStream_t)stream : c->own_stream;
+  free_graph(c);
+  return IB_OK;
+}
+
+int ib_set_option(ib_ctx *c, int32_t opt, int64_t value) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  switch (opt) {
+    case IB_OPT_PRESSURE:
+      c->want_p = value != 0;
+      if (c->want_p && !c->pspec) {
+        CK(dalloc(&c->pspec, (size_t)c->g.N * c->g.N * c->g.P));
+        CK(dalloc(&c->p, (size_t)c->g.V));
+      }
+      return IB_OK;
+    case IB_OPT_STAGE_TIMING: c->timing = value != 0; return IB_OK;
+    case IB_OPT_GRAPH: c->use_graph = value != 0; free_graph(c); return IB_OK;
+    default: return fail(IB_EINVAL, "unknown option");
+  }
+}
+
+int ib_set_structure(ib_ctx *c, const double *points, int64_t np, const ib_patch *patches,
+                     int32_t npatch, const double *stiffness, int64_t nstiff) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (np < 0 || npatch < 0 || nstiff < 0) return fail(IB_EINVAL, "negative count");
+  if ((np > 0 && (!points || !patches)) || (nstiff > 0 && !stiffness))
+    return fail(IB_EINVAL, "NULL array with non-zero count");
+  if (np > 0 && npatch == 0) return fail(IB_EINVAL, "points without patches");
+  if (np >= (int64_t)1 << 31) return fail(IB_EINVAL, "too many points");
+  std::vector<double> X, S;
+  std::vector<ib_patch> P;
+  CK(to_host(X, points, (size_t)np * 3, c->stream));
+  CK(to_host(P, patches, (size_t)npatch, c->stream));
+  CK(to_host(S, stiffness, (size_t)nstiff, c->stream));
+  for (int64_t i = 0; i < 3 * np; ++i)
+    if (!std::isfinite(X[i])) return fail(IB_EINVAL, "non-finite position at point " + std::to_string(i / 3));
+  int64_t next = 0;
+  for (int32_t p = 0; p < npatch; ++p) {
+    const ib_patch &q = P[p];
+    const std::string tag = "patch " + std::to_string(p) + ": ";
+    if (q.first != next) return fail(IB_EINVAL, tag + "patches must tile [0, np) in order");
+    if (q.n1 < 1 || q.n2 < 1) return fail(IB_EINVAL, tag + "n1, n2 must be >= 1");
+    if (q.flags & ~127u) return fail(IB_EINVAL, tag + "unknown flag bits");
+    if (q.pad_ != 0) return fail(IB_EINVAL, tag + "pad_ must be 0");
+    const int64_t npts = (int64_t)q.n1 * q.n2;
+    next += npts;
+    int nfam = 0;
+    for (int f = 0; f < 4; ++f) nfam += (q.flags >> (2 + f)) & 1;
+    const int64_t need = 2 * nfam * npts + ((q.flags & IB_TETHER) ? 4 * npts : 0);
+    if (q.param_off < 0 || q.param_off + need > nstiff) return fail(IB_EINVAL, tag + "stiffness block out of range");
+    for (int64_t k = 0; k < need; ++k)
+      if (!std::isfinite(S[q.param_off + k])) return fail(IB_EINVAL, tag + "non-finite stiffness at offset " + std::to_string(q.param_off + k));
+    // zero-length links at the given positions
+    int64_t b = q.param_off;
+    for (int f = 0; f < 4; ++f) {
+      if (!(q.flags & (IB_STRETCH1 << f))) continue;
+      const bool ax1 = (f & 1) == 0;
+      const int off = f < 2 ? 1 : 2;
+      const int n = ax1 ? q.n1 : q.n2;
+      const bool wrap = (q.flags & (ax1 ? IB_WRAP1 : IB_WRAP2)) != 0;
+      for (int32_t i2 = 0; i2 < q.n2; ++i2)
+        for (int32_t i1 = 0; i1 < q.n1; ++i1) {
+          const int cidx = ax1 ? i1 : i2;
+          if (!(cidx + off < n || wrap)) continue;
+          const int cf = (cidx + off) % n;
+          const int64_t li = (int64_t)i2 * q.n1 + i1;
+          const int64_t lj = ax1 ? (int64_t)i2 * q.n1 + cf : (int64_t)cf * q.n1 + i1;
+          const double *a = &X[3 * (q.first + li)], *bb = &X[3 * (q.first + lj)];
+          if (a[0] == bb[0] && a[1] == bb[1] && a[2] == bb[2])
+            return fail(IB_EDEGENERATE, tag + "zero-length link between points " +
+                                            std::to_string(q.first + li) + " and " +
+                                            std::to_string(q.first + lj));
+        }
+      b += 2 * (int64_t)q.n1 * q.n2;
+    }
+  }
+  if (next != np) return fail(IB_EINVAL, "patches cover " + std::to_string(next) + " points, np = " + std::to_string(np));
+  // upload
+  free_graph(c);
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c->X); dfree(c->patches); dfree(c->stiff);
+  c->X = nullptr; c->patches = nullptr; c->stiff = nullptr;
+  CK(dalloc(&c->X, (size_t)np * 3));
+  CK(dalloc(&c->patches, (size_t)npatch));
+  CK(dalloc(&c->stiff, (size_t)nstiff));
+  CK(copy_sync(c->X, X.data(), X.size() * sizeof(double), c->stream));
+  CK(copy_sync(c->patches, P.data(), P.size() * sizeof(ib_patch), c->stream));
+  CK(copy_sync(c->stiff, S.data(), S.size() * sizeof(double), c->stream));
+  c->np = np; c->npatch = npatch; c->nstiff = nstiff; c->patches_h = P;
+  // a drive that no longer fits is dropped
+  if (c->nd > 0) { dfree(c->drive_idx); dfree(c->drive_dir); c->drive_idx = nullptr; c->drive_dir = nullptr; c->nd = 0; }
+  return IB_OK;
+}
+
+int ib_set_positions(ib_ctx *c, const double *points) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (c->np == 0) return IB_OK;
+  if (!points) return fail(IB_EINVAL, "points is NULL");
+  CK(copy_sync(c->X, points, (size_t)c->np * 3 * sizeof(double), c->stream));
+  unsigned long long bad = 0;
+  int rc = count_nonfinite(c, c->X, (size_t)c->np * 3, &bad);
+  if (rc) return rc;
+  if (bad) return fail(IB_EINVAL, "non-finite positions");
+  return IB_OK;
+}
+
+int ib_set_velocity(ib_ctx *c, const double *u) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (!u) return fail(IB_EINVAL, "u is NULL");
+  CK(copy_sync(c->u, u, (size_t)3 * c->g.V * sizeof(double), c->stream));
+  unsigned long long bad = 0;
+  int rc = count_nonfinite(c, c->u, (size_t)3 * c->g.V, &bad);
+  if (rc) return rc;
+  if (bad) return fail(IB_EINVAL, "non-finite velocity");
+  c->have_p = false;
+  return IB_OK;
+}
+
+int ib_set_drive(ib_ctx *c, const int64_t *idx, int64_t n, const double *dir,
+                 double amp_per_point, int32_t period_steps) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(IB_EINVAL, "negative drive count");
+  if (n > 0) {
+    if (!idx || !dir) return fail(IB_EINVAL, "NULL drive arrays");
+    if (period_steps < 1) return fail(IB_EINVAL, "period_steps must be >= 1");
+    if (!std::isfinite(amp_per_point)) return fail(IB_EINVAL, "non-finite amplitude");
+    std::vector<int64_t> I;
+    std::vector<double> D;
+    CK(to_host(I, idx, (size_t)n, c->stream));
+    CK(to_host(D, dir, (size_t)n * 3, c->stream));
+    for (int64_t d = 0; d < n; ++d) {
+      if (I[d] < 0 || I[d] >= c->np) return fail(IB_EINVAL, "drive index out of range: " + std::to_string(I[d]));
+      for (int k = 0; k < 3; ++k)
+        if (!std::isfinite(D[3 * d + k])) return fail(IB_EINVAL, "non-finite drive direction");
+    }
+    free_graph(c);
+    CK(cudaStreamSynchronize(c->stream));
+    dfree(c->drive_idx); dfree(c->drive_dir);
+    c->drive_idx = nullptr; c->drive_dir = nullptr;
+    CK(dalloc(&c->drive_idx, (size_t)n));
+    CK(dalloc(&c->drive_dir, (size_t)n * 3));
+    CK(copy_sync(c->drive_idx, I.data(), I.size() * sizeof(int64_t), c->stream));
+    CK(copy_sync(c->drive_dir, D.data(), D.size() * sizeof(double), c->stream));
+  } else {
+    free_graph(c);
+  }
+  c->nd = n;
+  c->drive_amp = amp_per_point;
+  c->drive_period = n > 0 ? period_steps : 1;
+  return IB_OK;
+}
+
+int ib_step(ib_ctx *c, int32_t nsteps) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (nsteps < 0) return fail(IB_EINVAL, "nsteps < 0");
+  if (nsteps == 0) return IB_OK;
+  cudaStream_t s = c->stream;
+  *c->flag_h = LLONG_MAX;
+  CK(cudaMemcpyAsync(c->flag, c->flag_h, sizeof(long long), cudaMemcpyHostToDevice, s));
+  const bool timing = c->timing;
+  const size_t per = STAGE_COUNT + 1;
+  if (timing) {
+    while (c->ev_pool.size() < (size_t)nsteps * per) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      c->ev_pool.push_back(e);
+    }
+  }
+  for (int32_t k = 0; k < nsteps; ++k) {
+    const bool pressure = c->want_p && k == nsteps - 1;
+    CK(enqueue_step(c, pressure, nullptr, c->n + k, timing ? &c->ev_pool[k * per] : nullptr));
+    c->launches += launches_per_step(c);
+  }
+  CK(cudaMemcpyAsync(c->flag_h, c->flag, sizeof(long long), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  if (timing) {
+    for (int32_t k = 0; k < nsteps; ++k)
+      for (int st = 0; st < STAGE_COUNT; ++st) {
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev_pool[k * per + st], c->ev_pool[k * per + st + 1]));
+        c->stage_ms[st] += ms;
+      }
+  }
+  const long long bad = *c->flag_h;
+  c->have_p = c->want_p;
+  if (bad != LLONG_MAX) {
+    c->n = bad + 1;
+    return fail(IB_ENONFINITE, "non-finite u or X at step " + std::to_string(bad));
+  }
+  c->n += nsteps;
+  return IB_OK;
+}
+
+int ib_get_fields(ib_ctx *c, double *u, double *p) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (u) CK(copy_sync(u, c->u, (size_t)3 * c->g.V * sizeof(double), c->stream));
+  if (p) {
+    if (!c->have_p || !c->pspec) return fail(IB_ESTATE, "pressure not available: enable IB_OPT_PRESSURE before ib_step");
+    CK(launch_ypass(c->g, +1, c->pspec, 1, c->twN, c->stream));
+    CK(launch_xinv(c->g, c->pspec, c->p, 1, c->twN, c->twM, nullptr, nullptr, 0, c->stream));
+    c->launches += 2;
+    CK(copy_sync(p, c->p, (size_t)c->g.V * sizeof(double), c->stream));
+    c->have_p = false;    // pspec was transformed in place
+  }
+  return IB_OK;
+}
+
+int ib_get_positions(ib_ctx *c, double *X) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (c->np == 0) return IB_OK;
+  if (!X) return fail(IB_EINVAL, "X is NULL");
+  CK(copy_sync(X, c->X, (size_t)c->np * 3 * sizeof(double), c->stream));
+  return IB_OK;
+}
+
+int64_t ib_get_step(ib_ctx *c) { return c ? c->n : -1; }
+int ib_set_step(ib_ctx *c, int64_t n) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (n < 0) return fail(IB_EINVAL, "n < 0");
+  c->n = n;
+  return IB_OK;
+}
+int64_t ib_num_points(ib_ctx *c) { return c ? c->np : -1; }
+
+int ib_stage_times(ib_ctx *c, double *ms, int32_t cap, char *names, int32_t names_cap,
+                   int32_t reset) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  static const char *nm[STAGE_COUNT] = {"force_spread", "xfwd_rhs_r2c", "y_fwd", "z_solve",
+                                        "y_inv", "xinv_c2r", "interp_update"};
+  const int n = cap < STAGE_COUNT ? cap : STAGE_COUNT;
+  for (int k = 0; k < n; ++k) if (ms) ms[k] = c->stage_ms[k];
+  if (names && names_cap > 0) {
+    int pos = 0;
+    for (int k = 0; k < n; ++k) {
+      const int L = (int)strlen(nm[k]);
+      if (pos + L + 1 > names_cap) break;
+      memcpy(names + pos, nm[k], L + 1);
+      pos += L + 1;
+    }
+  }
+  if (reset) for (int k = 0; k < STAGE_COUNT; ++k) c->stage_ms[k] = 0.0;
+  return n;
+}
+
+int64_t ib_launch_count(ib_ctx *c, int32_t reset) {
+  if (!c) return -1;
+  const int64_t v = c->launches;
+  if (reset) c->launches = 0;
+  return v;
+}
+
+// ------------------------------------------------------------------ debug entry points
+
+int ib_debug_force(ib_ctx *c, double *f_out) {
+  if (!c || !f_out) return fail(IB_EINVAL, "NULL argument");
+  if (c->np == 0) return IB_OK;
+  Tmp t; double *f;
+  CK(t.get(&f, (size_t)c->np * 3));
+  CK(launch_force(struct_dev(c), nullptr, c->n, f, c->stream));
+  CK(copy_sync(f_out, f, (size_t)c->np * 3 * sizeof(double), c->stream));
+  return IB_OK;
+}
+
+int ib_debug_spread(ib_ctx *c, const double *f_node, double *F_out) {
+  if (!c || !f_node || !F_out) return fail(IB_EINVAL, "NULL argument");
+  Tmp t; double *f, *F;
+  const size_t V = (size_t)c->g.V;
+  CK(t.get(&F, 3 * V));
+  CK(cudaMemsetAsync(F, 0, 3 * V * sizeof(double), c->stream));
+  if (c->np > 0) {
+    CK(t.get(&f, (size_t)c->np * 3));
+    CK(copy_sync(f, f_node, (size_t)c->np * 3 * sizeof(double), c->stream));
+    CK(launch_force_spread(struct_dev(c), c->g, f, nullptr, c->n, F, c->stream));
+  }
+  CK(copy_sync(F_out, F, 3 * V * sizeof(double), c->stream));
+  return IB_OK;
+}
+
+int ib_debug_interp(ib_ctx *c, const double *u, double *U_out) {
+  if (!c || !u || !U_out) return fail(IB_EINVAL, "NULL argument");
+  if (c->np == 0) return IB_OK;
+  Tmp t; double *ud, *U;
+  const size_t V = (size_t)c->g.V;
+  CK(t.get(&ud, 3 * V));
+  CK(t.get(&U, (size_t)c->np * 3));
+  CK(copy_sync(ud, u, 3 * V * sizeof(double), c->stream));
+  CK(launch_interp(c->g, ud, c->X, c->np, U, nullptr, nullptr, 0, c->stream));
+  CK(copy_sync(U_out, U, (size_t)c->np * 3 * sizeof(double), c->stream));
+  return IB_OK;
+}
+
+int ib_debug_rhs(ib_ctx *c, const double *u, const double *F, double *r_out) {
+  if (!c || !u || !F || !r_out) return fail(IB_EINVAL, "NULL argument");
+  Tmp t; double *ud, *Fd, *r;
+  const size_t V = (size_t)c->g.V;
+  CK(t.get(&ud, 3 * V)); CK(t.get(&Fd, 3 * V)); CK(t.get(&r, 3 * V));
+  CK(copy_sync(ud, u, 3 * V * sizeof(double), c->stream));
+  CK(copy_sync(Fd, F, 3 * V * sizeof(double), c->stream));
+  CK(launch_xfwd(c->g, 1, ud, Fd, nullptr, r, c->spec, 3, c->twN, c->twM, c->stream));
+  CK(copy_sync(r_out, r, 3 * V * sizeof(double), c->stream));
+  return IB_OK;
+}
+
+int ib_debug_fluid(ib_ctx *c, const double *u, const double *F, double *u_out, double *p_out) {
+  if (!c || !u || !F || !u_out) return fail(IB_EINVAL, "NULL argument");
+  Tmp t; double *ud, *Fd, *pd = nullptr; double2 *ps = nullptr;
+  const FluidGeom &g = c->g;
+  const size_t V = (size_t)g.V;
+  cudaStream_t s = c->stream;
+  CK(t.get(&ud, 3 * V)); CK(t.get(&Fd, 3 * V));
+  if (p_out) { CK(t.get(&ps, (size_t)g.N * g.N * g.P)); CK(t.get(&pd, V)); }
+  CK(copy_sync(ud, u, 3 * V * sizeof(double), s));
+  CK(copy_sync(Fd, F, 3 * V * sizeof(double), s));
+  CK(launch_xfwd(g, 0, ud, Fd, nullptr, nullptr, c->spec, 3, c->twN, c->twM, s));
+  CK(launch_ypass(g, -1, c->spec, 3, c->twN, s));
+  CK(launch_zpass(g, 0, c->spec, ps, c->twN, c->sym_s, c->sym_l, s));
+  CK(launch_ypass(g, +1, c->spec, 3, c->twN, s));
+  CK(launch_xinv(g, c->spec, ud, 3, c->twN, c->twM, nullptr, nullptr, 0, s));
+  if (p_out) {
+    CK(launch_ypass(g, +1, ps, 1, c->twN, s));
+    CK(launch_xinv(g, ps, pd, 1, c->twN, c->twM, nullptr, nullptr, 0, s));
+    CK(copy_sync(p_out, pd, V * sizeof(double), s));
+  }
+  CK(copy_sync(u_out, ud, 3 * V * sizeof(double), s));
+  return IB_OK;
+}
+
+int ib_debug_fft(ib_ctx *c, const double *in, double *out) {
+  if (!c || !in || !out) return fail(IB_EINVAL, "NULL argument");
+  Tmp t; double *ind;
+  const FluidGeom &g = c->g;
+  const size_t V = (size_t)g.V;
+  cudaStream_t s = c->stream;
+  CK(t.get(&ind, V));
+  CK(copy_sync(ind, in, V * sizeof(double), s));
+  CK(launch_xfwd(g, 2, nullptr, nullptr, ind, nullptr, c->spec, 1, c->twN, c->twM, s));
+  CK(launch_ypass(g, -1, c->spec, 1, c->twN, s));
+  CK(launch_zpass(g, 1, c->spec, nullptr, c->twN, c->sym_s, c->sym_l, s));
+  CK(cudaMemcpy2DAsync(out, (size_t)(g.M + 1) * 2 * sizeof(double), c->spec,
+                       (size_t)g.P * sizeof(double2), (size_t)(g.M + 1) * sizeof(double2),
+                       (size_t)g.N * g.N, cudaMemcpyDefault, s));
+  CK(cudaStreamSynchronize(s));
+  return IB_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// ib_internal.cuh — context layout and kernel launchers of the B200 IB step.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/ib.h"
+
+namespace ibk {
+
+// Device view of the Lagrangian structure (all pointers device memory).
+struct StructDev {
+  const double *X;            // [np][3]
+  int64_t np;
+  const ib_patch *patches;    // [npatch]
+  int32_t npatch;
+  const double *stiff;
+  int64_t nd;                 // drive
+  const int64_t *drive_idx;
+  const double *drive_dir;
+  double drive_amp;
+  int32_t drive_period;
+};
+
+// Per-N launch configuration of the fluid passes.
+struct FluidGeom {
+  int N, M, P;                // M = N/2; P = spectrum row pitch in complex (>= M+1)
+  int64_t V;
+  double h, invh, rho, mu, dt;
+};
+
+enum { STAGE_FORCE_SPREAD = 0, STAGE_XFWD, STAGE_YFWD, STAGE_ZPROJ, STAGE_YINV, STAGE_XINV,
+       STAGE_INTERP, STAGE_COUNT };
+
+}  // namespace ibk
+
+struct ib_ctx {
+  ibk::FluidGeom g;
+  cudaStream_t stream = nullptr;
+  cudaStream_t own_stream = nullptr;
+  // Eulerian state and work arrays
+  double *u = nullptr;          // [3][V]
+  double *F = nullptr;          // [3][V]  (kept zero between steps)
+  double2 *spec = nullptr;      // [3][N][N][P]
+  double2 *pspec = nullptr;     // [N][N][P]  (pressure, lazily)
+  double *p = nullptr;          // [V] pressure output cache (lazily)
+  double2 *twN = nullptr, *twM = nullptr;   // exp(-2 pi i t/L) tables
+  double *sym_s = nullptr, *sym_l = nullptr; // per-axis symbols
+  // Lagrangian state
+  int64_t np = 0;
+  double *X = nullptr;
+  ib_patch *patches = nullptr;
+  int32_t npatch = 0;
+  double *stiff = nullptr;
+  int64_t nstiff = 0;
+  std::vector<ib_patch> patches_h;
+  int64_t nd = 0;
+  int64_t *drive_idx = nullptr;
+  double *drive_dir = nullptr;
+  double drive_amp = 0.0;
+  int32_t drive_period = 1;
+  // control
+  int64_t n = 0;
+  long long *flag = nullptr;    // device: first non-finite step (LLONG_MAX = none)
+  long long *flag_h = nullptr;  // pinned
+  bool want_p = false, have_p = false, timing = false, use_graph = true;
+  cudaEvent_t ev[ibk::STAGE_COUNT + 1] = {};
+  double stage_ms[ibk::STAGE_COUNT] = {};
+  std::vector<cudaEvent_t> ev_pool;   // per-step stage events (IB_OPT_STAGE_TIMING)
+  int64_t launches = 0;
+  // CUDA graph of one step (valid while graph_key matches)
+  cudaGraphExec_t graph = nullptr;
+  long long graph_key = -1;
+  long long *dev_n = nullptr;   // device step counter used by graph replays
+};
+
+namespace ibk {
+// kernels/launchers (fluid.cu)
+cudaError_t init_tables(ib_ctx *c);
+cudaError_t fluid_setup_attributes(int N);
+// x pass: mode 0 = step (r from u,F; zero F), 1 = r only (write r_out), 2 = FFT of in (1 comp)
+cudaError_t launch_xfwd(const FluidGeom &g, int mode, const double *u, double *F,
+                        const double *in, double *r_out, double2 *spec, int ncomp,
+                        const double2 *twN, const double2 *twM, cudaStream_t s);
+cudaError_t launch_ypass(const FluidGeom &g, int sign, double2 *spec, int ncomp,
+                         const double2 *twN, cudaStream_t s);
+// z pass: mode 0 = fwd+project+inv (pressure if pspec != null), 1 = forward only
+cudaError_t launch_zpass(const FluidGeom &g, int mode, double2 *spec, double2 *pspec,
+                         const double2 *twN, const double *sym_s, const double *sym_l,
+                         cudaStream_t s);
+cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, int ncomp,
+                        const double2 *twN, const double2 *twM, long long *flag,
+                        const long long *dev_n, long long n, cudaStream_t s);
+// Lagrangian kernels (lagrangian.cu)
+cudaError_t launch_force(const StructDev &sd, const long long *dev_n, long long n,
+                         double *f_out, cudaStream_t s);
+cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g,
+                                const double *f_in, const long long *dev_n, long long n,
+                                double *F, cudaStream_t s);
+cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
+                          double *U_out, long long *flag, const long long *dev_n, long long n,
+                          cudaStream_t s);
+}  // namespace ibk

@@ -1,0 +1,287 @@
+// lagrangian.cu — steps 1, 2 and 4 of the IB step on sm_100a.
+//
+//   force  (PAPER.md 610-616): per-point gather over the incident links of its structured
+//          patch (stretch / bend springs), tether and drive; nodal forces (Z12).
+//   spread (eq:discreteF, PAPER.md 712-723): the force is computed in registers and
+//          spread with Peskin's 4-point delta (745-759).  Lanes of a warp whose support
+//          boxes coincide (same base cell) are merged: their 12 weights + force go to
+//          shared memory, the warp's 32 lanes then own the 64 nodes x 3 components of the
+//          box (6 outputs per lane), sum the group's contributions in registers and flush
+//          once with fp64 atomicAdd — one atomic per (group, node, component) instead of
+//          one per (point, node, component).
+//   interp + update (eq:discreteX, PAPER.md 725-734): gather of u^{n+1} at X^n fused with
+//          X^{n+1} = X^n + dt U, with a non-finite check.
+#include <climits>
+
+#include "ib_internal.cuh"
+
+namespace ibk {
+
+// ------------------------------------------------------------------ delta weights
+// Window j0 = floor(X/h) - 1 .. +2 (Z8); with f = X/h - floor(X/h) in [0,1):
+//   phi(-f)   = (3 - 2f + sqrt(1 + 4f - 4f^2))/8           (|r| <= 1 branch)
+//   phi(1-f)  = (1 + 2f + sqrt(1 + 4f - 4f^2))/8           (same root)
+//   phi(1+f)  = 1/2 - phi(1-f),  phi(2-f) = 1/2 - phi(-f)  (1 <= |r| <= 2 branch)
+__device__ __forceinline__ int axis_weights(double Xa, double invh, double w[4]) {
+  const double s = Xa * invh;
+  const double fl = floor(s);
+  const double f = s - fl;
+  const double q = sqrt(1.0 + 4.0 * f - 4.0 * f * f);
+  w[1] = (3.0 - 2.0 * f + q) * 0.125;
+  w[2] = (1.0 + 2.0 * f + q) * 0.125;
+  w[0] = 0.5 - w[2];
+  w[3] = 0.5 - w[1];
+  return (int)(long long)fl - 1;
+}
+
+// ------------------------------------------------------------------ force
+__device__ __forceinline__ void spring(const double *__restrict__ X, double xi, double yi,
+                                       double zi, int64_t j, double k, double L0, double f[3]) {
+  const double dx = __ldg(&X[3 * j + 0]) - xi;
+  const double dy = __ldg(&X[3 * j + 1]) - yi;
+  const double dz = __ldg(&X[3 * j + 2]) - zi;
+  // |d| in plain IEEE order without contraction (Z13): exactly L0 at rest
+  const double len = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)),
+                                          __dmul_rn(dz, dz)));
+  const double t = k * (len - L0) / len;
+  f[0] += t * dx;
+  f[1] += t * dy;
+  f[2] += t * dz;
+}
+
+__device__ __forceinline__ void point_force(const StructDev &sd, int64_t i, double f[3]) {
+  int lo = 0, hi = sd.npatch - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (__ldg(&sd.patches[mid].first) <= i) lo = mid; else hi = mid - 1;
+  }
+  const ib_patch *P = sd.patches + lo;
+  const int64_t first = __ldg(&P->first);
+  const int n1 = __ldg(&P->n1), n2 = __ldg(&P->n2);
+  const uint32_t fl = __ldg(&P->flags);
+  const int64_t npts = (int64_t)n1 * n2;
+  const int64_t li = i - first;
+  const int i1 = (int)(li % n1), i2 = (int)(li / n1);
+  const double *b = sd.stiff + __ldg(&P->param_off);
+  const double xi = __ldg(&sd.X[3 * i + 0]), yi = __ldg(&sd.X[3 * i + 1]),
+               zi = __ldg(&sd.X[3 * i + 2]);
+  f[0] = f[1] = f[2] = 0.0;
+#pragma unroll
+  for (int fam = 0; fam < 4; ++fam) {
+    const uint32_t bit = (uint32_t)IB_STRETCH1 << fam;
+    if (!(fl & bit)) continue;
+    const double *k = b, *L0 = b + npts;
+    b += 2 * npts;
+    const bool ax1 = (fam & 1) == 0;
+    const int off = fam < 2 ? 1 : 2;
+    const int n = ax1 ? n1 : n2, c = ax1 ? i1 : i2;
+    const bool wrap = (fl & (ax1 ? IB_WRAP1 : IB_WRAP2)) != 0;
+    int cf = c + off;
+    if (cf < n || wrap) {
+      cf %= n;
+      const int64_t lj = ax1 ? (int64_t)i2 * n1 + cf : (int64_t)cf * n1 + i1;
+      spring(sd.X, xi, yi, zi, first + lj, __ldg(&k[li]), __ldg(&L0[li]), f);
+    }
+    int cb = c - off;
+    if (cb >= 0 || wrap) {
+      cb = (cb % n + n) % n;
+      const int64_t lj = ax1 ? (int64_t)i2 * n1 + cb : (int64_t)cb * n1 + i1;
+      spring(sd.X, xi, yi, zi, first + lj, __ldg(&k[lj]), __ldg(&L0[lj]), f);
+    }
+  }
+  if (fl & IB_TETHER) {
+    const double kt = __ldg(&b[li]);
+    const double *Y = b + npts;
+    f[0] += kt * (__ldg(&Y[3 * li + 0]) - xi);
+    f[1] += kt * (__ldg(&Y[3 * li + 1]) - yi);
+    f[2] += kt * (__ldg(&Y[3 * li + 2]) - zi);
+  }
+}
+
+__device__ __forceinline__ double drive_factor(const StructDev &sd, long long n) {
+  const long long T = sd.drive_period;
+  return sd.drive_amp * sinpi(2.0 * (double)(n % T) / (double)T);
+}
+
+__global__ void k_force(StructDev sd, const long long *dev_n, long long n, double *f_out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= sd.np) return;
+  double f[3];
+  point_force(sd, i, f);
+  f_out[3 * i + 0] = f[0];
+  f_out[3 * i + 1] = f[1];
+  f_out[3 * i + 2] = f[2];
+}
+
+__global__ void k_drive_add(StructDev sd, const long long *dev_n, long long n, double *f_out) {
+  const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= sd.nd) return;
+  const double a = drive_factor(sd, dev_n ? *dev_n : n);
+  const int64_t i = sd.drive_idx[d];
+  for (int c = 0; c < 3; ++c) f_out[3 * i + c] += a * sd.drive_dir[3 * d + c];
+}
+
+// Spread of the drive forces (few points): one thread per point, 192 atomics.
+__global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n, long long n,
+                               double *F) {
+  const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (d >= sd.nd) return;
+  const int N = g.N;
+  const size_t V = (size_t)g.V;
+  const double a = drive_factor(sd, dev_n ? *dev_n : n) * g.invh * g.invh * g.invh;
+  if (a == 0.0) return;
+  const int64_t i = sd.drive_idx[d];
+  double wx[4], wy[4], wz[4];
+  const int jx = axis_weights(sd.X[3 * i + 0], g.invh, wx);
+  const int jy = axis_weights(sd.X[3 * i + 1], g.invh, wy);
+  const int jz = axis_weights(sd.X[3 * i + 2], g.invh, wz);
+  const double fd[3] = {a * sd.drive_dir[3 * d], a * sd.drive_dir[3 * d + 1],
+                        a * sd.drive_dir[3 * d + 2]};
+  for (int c = 0; c < 4; ++c)
+    for (int b = 0; b < 4; ++b)
+      for (int e = 0; e < 4; ++e) {
+        const size_t cell = ((size_t)((jz + c) & (N - 1)) * N + ((jy + b) & (N - 1))) * N +
+                            ((jx + e) & (N - 1));
+        const double w = wx[e] * wy[b] * wz[c];
+        for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], fd[k] * w);
+      }
+}
+
+// ------------------------------------------------------------------ force + spread
+constexpr int SPREAD_THREADS = 256;
+constexpr int REC = 17;    // 12 weights + 3 forces, padded to an odd stride (bank spread)
+
+template <bool FROM_ARRAY>
+__global__ void __launch_bounds__(SPREAD_THREADS)
+k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, double *F) {
+  __shared__ double rec[SPREAD_THREADS / 32][32][REC];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int N = g.N;
+  const size_t V = (size_t)g.V;
+  double *r = rec[warp][lane];
+  unsigned key = 0xffffffffu;
+  bool live = false;
+  if (i < sd.np) {
+    double f[3];
+    if (FROM_ARRAY) {
+      f[0] = __ldg(&f_in[3 * i]); f[1] = __ldg(&f_in[3 * i + 1]); f[2] = __ldg(&f_in[3 * i + 2]);
+    } else {
+      point_force(sd, i, f);
+    }
+    const double ih3 = g.invh * g.invh * g.invh;
+    live = (f[0] != 0.0) || (f[1] != 0.0) || (f[2] != 0.0);
+    const int jx = axis_weights(__ldg(&sd.X[3 * i + 0]), g.invh, r + 0) & (N - 1);
+    const int jy = axis_weights(__ldg(&sd.X[3 * i + 1]), g.invh, r + 4) & (N - 1);
+    const int jz = axis_weights(__ldg(&sd.X[3 * i + 2]), g.invh, r + 8) & (N - 1);
+    r[12] = f[0] * ih3; r[13] = f[1] * ih3; r[14] = f[2] * ih3;
+    key = ((unsigned)jz * N + (unsigned)jy) * N + (unsigned)jx;
+  }
+  __syncwarp();
+  unsigned todo = __ballot_sync(0xffffffffu, live);
+  // lane -> outputs (a, b, c0 | c0 + 2, component 0..2)
+  const int a = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
+  while (todo) {
+    const int leader = __ffs(todo) - 1;
+    const unsigned kl = __shfl_sync(0xffffffffu, key, leader);
+    const unsigned grp = __ballot_sync(0xffffffffu, key == kl) & todo;
+    todo &= ~grp;
+    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+    unsigned m = grp;
+    while (m) {
+      const int p = __ffs(m) - 1;
+      m &= m - 1;
+      const double *q = rec[warp][p];
+      const double wab = q[a] * q[4 + b];
+      const double w0 = wab * q[8 + c0], w1 = wab * q[10 + c0];
+      acc[0] += q[12] * w0; acc[1] += q[12] * w1;
+      acc[2] += q[13] * w0; acc[3] += q[13] * w1;
+      acc[4] += q[14] * w0; acc[5] += q[14] * w1;
+    }
+    const unsigned jx = kl % N, jy = (kl / N) % N, jz = kl / (N * N);
+    const size_t x = (jx + a) & (N - 1), y = (jy + b) & (N - 1);
+    const size_t z0 = (jz + c0) & (N - 1), z1 = (jz + c0 + 2) & (N - 1);
+    const size_t e0 = (z0 * N + y) * N + x, e1 = (z1 * N + y) * N + x;
+    atomicAdd(&F[e0], acc[0]);          atomicAdd(&F[e1], acc[1]);
+    atomicAdd(&F[V + e0], acc[2]);      atomicAdd(&F[V + e1], acc[3]);
+    atomicAdd(&F[2 * V + e0], acc[4]);  atomicAdd(&F[2 * V + e1], acc[5]);
+  }
+}
+
+cudaError_t launch_force(const StructDev &sd, const long long *dev_n, long long n,
+                         double *f_out, cudaStream_t s) {
+  if (sd.np > 0) k_force<<<(unsigned)((sd.np + 255) / 256), 256, 0, s>>>(sd, dev_n, n, f_out);
+  if (sd.nd > 0) k_drive_add<<<(unsigned)((sd.nd + 127) / 128), 128, 0, s>>>(sd, dev_n, n, f_out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const double *f_in,
+                                const long long *dev_n, long long n, double *F,
+                                cudaStream_t s) {
+  const unsigned blocks = (unsigned)((sd.np + SPREAD_THREADS - 1) / SPREAD_THREADS);
+  if (sd.np > 0) {
+    if (f_in)
+      k_force_spread<true><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F);
+    else
+      k_force_spread<false><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F);
+  }
+  if (!f_in && sd.nd > 0)
+    k_drive_spread<<<(unsigned)((sd.nd + 63) / 64), 64, 0, s>>>(sd, g, dev_n, n, F);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ interp + update
+__global__ void __launch_bounds__(256)
+k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
+         long long *flag, const long long *dev_n, long long n) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool bad = false;
+  if (i < np) {
+    const int N = g.N;
+    const size_t V = (size_t)g.V;
+    const double x0 = X[3 * i + 0], x1 = X[3 * i + 1], x2 = X[3 * i + 2];
+    double wx[4], wy[4], wz[4];
+    const int jx = axis_weights(x0, g.invh, wx);
+    const int jy = axis_weights(x1, g.invh, wy);
+    const int jz = axis_weights(x2, g.invh, wz);
+    double U0 = 0.0, U1 = 0.0, U2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const size_t z = (size_t)((jz + c) & (N - 1));
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const size_t row = (z * N + ((jy + b) & (N - 1))) * N;
+        const double wbc = wy[b] * wz[c];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const size_t cell = row + ((jx + e) & (N - 1));
+          const double w = wx[e] * wbc;
+          U0 += __ldg(&u[cell]) * w;
+          U1 += __ldg(&u[V + cell]) * w;
+          U2 += __ldg(&u[2 * V + cell]) * w;
+        }
+      }
+    }
+    if (U_out) {
+      U_out[3 * i + 0] = U0; U_out[3 * i + 1] = U1; U_out[3 * i + 2] = U2;
+    } else {
+      const double y0 = x0 + g.dt * U0, y1 = x1 + g.dt * U1, y2 = x2 + g.dt * U2;
+      X[3 * i + 0] = y0; X[3 * i + 1] = y1; X[3 * i + 2] = y2;
+      bad = !(isfinite(y0) && isfinite(y1) && isfinite(y2));
+    }
+  }
+  if (flag && __syncthreads_or(bad) && threadIdx.x == 0) {
+    const long long st = dev_n ? *dev_n - 1 : n;
+    atomicMin(flag, st);
+  }
+}
+
+cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
+                          double *U_out, long long *flag, const long long *dev_n, long long n,
+                          cudaStream_t s) {
+  if (np > 0)
+    k_interp<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(g, u, X, np, U_out, flag, dev_n, n);
+  return cudaGetLastError();
+}
+
+}  // namespace ibk

@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path through the C-ABI against the CPU oracle, element by element.
+
+Tolerances: single stages with a deterministic order 1e-13 relative;
+atomic stages (spread) 1e-13; full IB step rel-L2 <= 1e-11 after 1 step and <= 1e-9
+after 10 steps on u and X (BASELINE.json north_star), plus the interpolated velocity U
+and the displacement X - X0 (reading Z4).
+"""
+import numpy as np
+import pytest
+
+from gen import make_config, random_divfree_velocity, random_points, small_sheet_config
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ibm():
+    from paper_math_0301321_b200 import _build, ib
+    _build.build()
+    ib.load()
+    return ib
+
+
+def rel_l2(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    nb = np.linalg.norm(b)
+    na = np.linalg.norm(a - b)
+    if nb == 0.0:
+        return 0.0 if na == 0.0 else np.inf
+    return na / nb
+
+
+def _ctx(ibm, N, rho=1.0, mu=0.01, dt=1e-3, X=None, patches=None, stiff=None):
+    c = ibm.IBContext(N, 1.0 / N, rho, mu, dt)
+    if X is not None:
+        c.set_structure(X, patches, stiff)
+    return c
+
+
+def _points_only(X):
+    """A structure of free points (one patch, no links) so debug spread/interp see X."""
+    from gen import Patch
+    return [Patch(0, X.shape[0], 1, 0, 0)], np.zeros(0)
+
+
+# ------------------------------------------------------------------ single stages
+@pytest.mark.parametrize("N", [8, 16, 32, 64, 128])
+def test_fft_matches_oracle_and_numpy(ibm, olib, N):
+    rng = np.random.default_rng(N)
+    x = rng.standard_normal((N, N, N))
+    with _ctx(ibm, N) as c:
+        got = c.debug_fft(x)
+    ref = np.fft.rfftn(x)
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref)) * np.log2(N)
+    if N <= 32:
+        orc = olib.fft3(x.astype(complex), -1)[:, :, : N // 2 + 1]
+        assert np.max(np.abs(got - orc)) < 1e-13 * np.max(np.abs(orc)) * np.log2(N)
+
+
+@pytest.mark.parametrize("N", [8, 16, 32])
+def test_rhs_matches_oracle(ibm, olib, N):
+    rng = np.random.default_rng(1)
+    u = rng.standard_normal((3, N, N, N))
+    u[0, 0, 0, :] = 0.0                      # ties u_k = 0 (reading Z5)
+    F = rng.standard_normal((3, N, N, N))
+    h, rho, dt = 1.0 / N, 1.3, 2e-3
+    with ibm.IBContext(N, h, rho, 0.01, dt) as c:
+        r = c.debug_rhs(u, F)
+    ref = olib.rhs(N, h, rho, dt, u, F)
+    assert np.max(np.abs(r - ref)) <= 1e-13 * np.max(np.abs(ref))
+
+
+@pytest.mark.parametrize("N", [8, 16, 32, 64])
+def test_fluid_step_matches_oracle(ibm, olib, N):
+    rng = np.random.default_rng(2)
+    u = random_divfree_velocity(N, 3, 0.3, rng) + 0.05 * rng.standard_normal((3, N, N, N))
+    F = rng.standard_normal((3, N, N, N)) * 50
+    h, rho, mu, dt = 1.0 / N, 1.0, 0.02, 1e-3
+    with ibm.IBContext(N, h, rho, mu, dt) as c:
+        un, p = c.debug_fluid(u, F)
+    ref_u, ref_p = olib.fluid_step(N, h, rho, mu, dt, u, F)
+    assert rel_l2(un, ref_u) < 1e-13
+    assert rel_l2(p, ref_p) < 1e-12
+
+
+@pytest.mark.parametrize("N,npts,cluster", [(16, 1000, False), (32, 5000, True), (64, 20000, True)])
+def test_spread_matches_oracle(ibm, olib, N, npts, cluster):
+    rng = np.random.default_rng(3)
+    if cluster:   # heavy per-cell fan-in (many points per cell) + points outside [0,1)
+        centres = rng.uniform(-0.2, 1.2, (npts // 50, 3))
+        X = centres[rng.integers(0, len(centres), npts)] + rng.uniform(0, 0.3 / N, (npts, 3))
+    else:
+        X = random_points(npts, rng)
+    f = rng.standard_normal((npts, 3))
+    f[::7] = 0.0
+    patches, st = _points_only(X)
+    with _ctx(ibm, N, X=X, patches=patches, stiff=st) as c:
+        F = c.debug_spread(f)
+    ref = olib.spread(N, 1.0 / N, X, f)
+    assert rel_l2(F, ref) < 1e-13
+    tot = F.reshape(3, -1).sum(1) / N ** 3
+    assert np.allclose(tot, f.sum(0), rtol=0, atol=1e-11 * np.abs(f).sum())
+
+
+@pytest.mark.parametrize("N,npts", [(16, 777), (64, 20000)])
+def test_interp_matches_oracle_and_adjoint(ibm, olib, N, npts):
+    rng = np.random.default_rng(4)
+    X = random_points(npts, rng, -0.5, 1.5)
+    u = rng.standard_normal((3, N, N, N))
+    patches, st = _points_only(X)
+    with _ctx(ibm, N, X=X, patches=patches, stiff=st) as c:
+        U = c.debug_interp(u)
+        f = rng.standard_normal((npts, 3))
+        F = c.debug_spread(f)
+    ref = olib.interp(N, 1.0 / N, u, X)
+    assert rel_l2(U, ref) < 1e-14
+    lhs = np.sum(F * u) / N ** 3
+    rhs = np.sum(f * U)
+    assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+
+
+@pytest.mark.parametrize("step", [0, 3, 5])
+def test_force_matches_oracle(ibm, olib, step):
+    cfg = small_sheet_config(N=16, n1=12, n2=10, seed=5)
+    with ibm.IBContext.from_config(cfg) as c:
+        c.set_step(step)
+        f = c.debug_force()
+    ref = olib.force(cfg.X, cfg.patches, cfg.stiffness, step, cfg.drive_idx, cfg.drive_dir,
+                     cfg.drive_amp, cfg.drive_period)
+    assert rel_l2(f, ref) < 1e-14
+
+
+def test_force_at_rest_is_exactly_zero(ibm):
+    cfg = make_config(3)
+    with ibm.IBContext.from_config(cfg) as c:
+        assert np.max(np.abs(c.debug_force())) == 0.0
+
+
+# ------------------------------------------------------------------ whole step
+def _parity(ibm, olib, cfg, steps=(1, 9), tol=(1e-11, 1e-9)):
+    o = olib.Oracle.from_config(cfg)
+    c = ibm.IBContext.from_config(cfg)
+    X0 = cfg.X.copy()
+    report = []
+    done = 0
+    for k, t in zip(steps, tol):
+        o.step(k)
+        c.step(k)
+        done += k
+        uo, _ = o.get_fields()
+        ug, _ = c.get_fields()
+        Xo, Xg = o.get_positions(), c.get_positions()
+        e_u, e_X = rel_l2(ug, uo), rel_l2(Xg, Xo)
+        e_d = rel_l2(Xg - X0, Xo - X0)
+        report.append((done, e_u, e_X, e_d))
+        assert e_u <= t, (cfg.name, done, "u", e_u)
+        assert e_X <= t, (cfg.name, done, "X", e_X)
+        # displacement: fp64 floor ~ ulp(max|X|)/rms|X - X0| (reading Z4)
+        disp = np.sqrt(np.mean((Xo - X0) ** 2))
+        floor = 8 * np.spacing(np.max(np.abs(X0))) / disp if disp > 0 else 0.0
+        assert e_d <= max(100 * t, 10 * floor), (cfg.name, done, "X-X0", e_d, floor)
+        assert c.n == o.n == done
+    c.close()
+    return report
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_config_step_parity(ibm, olib, k):
+    print(_parity(ibm, olib, make_config(k)))
+
+
+@pytest.mark.slow
+def test_config4_step_parity(ibm, olib):
+    print(_parity(ibm, olib, make_config(4)))
+
+
+@pytest.mark.parametrize("k", [1, 2])
+def test_interpolated_velocity_parity(ibm, olib, k):
+    """U at the step's positions (Z4): the high-precision check behind X."""
+    cfg = make_config(k)
+    o = olib.Oracle.from_config(cfg)
+    o.step(1)
+    u1, _ = o.get_fields()
+    with ibm.IBContext.from_config(cfg) as c:
+        c.step(1)
+        ug, _ = c.get_fields()
+        Ug = c.debug_interp(ug)            # at X^1 (positions after the step)
+    Uo = olib.interp(cfg.N, cfg.h, u1, o.get_positions())
+    assert rel_l2(Ug, Uo) < 1e-11
+
+
+def test_small_sheet_with_tethers_drive_and_flow(ibm, olib):
+    cfg = small_sheet_config(N=32, n1=20, n2=14, seed=6, u_amp=0.2)
+    rep = _parity(ibm, olib, cfg, steps=(1, 9), tol=(1e-11, 1e-9))
+    print(rep)
+
+
+def test_pure_fluid_and_pressure(ibm, olib):
+    N = 32
+    rng = np.random.default_rng(7)
+    u0 = random_divfree_velocity(N, 4, 0.5, rng)
+    o = olib.Oracle(N, 1.0 / N, 1.0, 0.01, 1e-3)
+    o.set_velocity(u0)
+    with ibm.IBContext(N, 1.0 / N, 1.0, 0.01, 1e-3) as c:
+        c.set_velocity(u0)
+        c.set_option(ibm.IB_OPT_PRESSURE, 1)
+        c.step(3)
+        o.step(3)
+        ug, pg = c.get_fields(want_p=True)
+    uo, po = o.get_fields()
+    assert rel_l2(ug, uo) < 1e-12
+    assert rel_l2(pg, po) < 1e-10
+
+
+def test_device_pointers_roundtrip(ibm):
+    import torch
+    cfg = make_config(1)
+    N = cfg.N
+    with ibm.IBContext.from_config(cfg) as c:
+        u = torch.randn(3, N, N, N, dtype=torch.float64, device="cuda") * 1e-3
+        c.set_velocity(u)
+        out = torch.empty_like(u)
+        c.get_fields_into(out)
+        assert torch.equal(out, u)
+        X = torch.empty(cfg.X.shape[0], 3, dtype=torch.float64, device="cuda")
+        c.get_positions_into(X)
+        assert np.array_equal(X.cpu().numpy(), cfg.X)
+
+
+def test_error_codes(ibm):
+    from gen import Patch, STRETCH1
+    with ibm.IBContext(16, 1 / 16, 1, 0.01, 1e-3) as c:
+        X = np.array([[0.5, 0.5, 0.5], [0.5, 0.5, 0.5]])
+        with pytest.raises(ibm.IBError) as e:
+            c.set_structure(X, [Patch(0, 2, 1, STRETCH1, 0)], np.array([1.0, 0, 0.1, 0]))
+        assert e.value.code == ibm.IB_EDEGENERATE
+        with pytest.raises(ibm.IBError) as e:
+            c.set_structure(np.array([[np.nan, 0, 0]]), [Patch(0, 1, 1, 0, 0)], np.zeros(0))
+        assert e.value.code == ibm.IB_EINVAL
+        with pytest.raises(ibm.IBError) as e:
+            c.get_fields(want_p=True)
+        assert e.value.code == ibm.IB_ESTATE
+        # blow-up is detected and reported
+        X = np.array([[0.5, 0.5, 0.5], [0.52, 0.5, 0.5]])
+        c.set_structure(X, [Patch(0, 2, 1, STRETCH1, 0)], np.array([1e30, 0, 1e-6, 0]))
+        with pytest.raises(ibm.IBError) as e:
+            c.step(50)
+        assert e.value.code == ibm.IB_ENONFINITE
+
+
+def test_empty_structure_and_smallest_grid(ibm, olib):
+    with ibm.IBContext(8, 1 / 8, 1.0, 0.1, 1e-2) as c:
+        c.step(2)
+        u, _ = c.get_fields()
+        assert np.max(np.abs(u)) == 0.0
+        assert c.get_positions().shape == (0, 3)
