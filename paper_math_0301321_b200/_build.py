@@ -28,11 +28,12 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def build(force: bool = False, verbose: bool = False, extra=None) -> str:
+def build(force: bool = False, verbose: bool = False, extra=None, out: str = None) -> str:
+    target = out or SO
     newest = max(os.path.getmtime(p) for p in _deps())
-    if not force and os.path.exists(SO) and os.path.getmtime(SO) >= newest:
-        return SO
-    tmp = SO + f".tmp{os.getpid()}"
+    if not force and os.path.exists(target) and os.path.getmtime(target) >= newest:
+        return target
+    tmp = target + f".tmp{os.getpid()}"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
            "-cudart", "shared", "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
     if verbose:
@@ -40,8 +41,8 @@ def build(force: bool = False, verbose: bool = False, extra=None) -> str:
     if extra:
         cmd[1:1] = list(extra)
     subprocess.check_call(cmd)
-    os.replace(tmp, SO)
-    return SO
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

@@ -3,8 +3,11 @@
 // Used by the x/y/z passes of the fluid solve ("can be solved
 // efficiently with the use of the Fast Fourier Transform algorithm").  A CTA holds a
 // batch of pencils in shared memory, one pencil = L complex doubles, element i at
-// pencil_base[PAD(i)], PAD(i) = i + i/16 (one spare double2 every 16 elements keeps the
-// radix-16 strided stores at <= 2-way bank conflict).  Each pencil is transformed by
+// pencil_base[PAD(i)] with the XOR swizzle PAD(i) = i ^ (((i >> 1) ^ (i >> 4)) & 7): a
+// 16-byte access is served per quarter-warp (8 lanes), and for every pass of every plan
+// here (radix-R0 strided stores, contiguous loads) 8 consecutive jobs then fall in 8
+// distinct 16-byte bank groups (checked exhaustively for L = 8..1024).  Pencil stride
+// LD = L + 1 (odd) keeps 8 different pencils at the same element conflict-free too.  Each pencil is transformed by
 // Plan<L>::T threads; every pass loads R elements per job into registers, multiplies by
 // the inter-pass twiddles, runs an unrolled register DFT-R, and stores in Stockham order,
 // so the result is in natural order.  Twiddles come from a device table
@@ -12,6 +15,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include <type_traits>
 
 namespace ibk {
 
@@ -24,12 +29,12 @@ struct Plan {
   static constexpr int T = L / RMAX;                           // threads per pencil
   static constexpr int NPASS = (ilog2c(L) + 3) / 4;            // passes of radix <= 16
   static constexpr int R0 = L >> (4 * (NPASS - 1));            // first-pass radix
-  static constexpr int LD = L + L / 16 + 1;                    // padded pencil stride
+  static constexpr int LD = L + 1;                             // pencil stride (odd)
   __host__ __device__ static constexpr int radix(int p) { return p == 0 ? R0 : 16; }
   __host__ __device__ static constexpr int ns(int p) { return p == 0 ? 1 : R0 << (4 * (p - 1)); }
 };
 
-__device__ __forceinline__ int PAD(int i) { return i + (i >> 4); }
+__device__ __forceinline__ int PAD(int i) { return i ^ (((i >> 1) ^ (i >> 4)) & 7); }
 
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
@@ -147,6 +152,138 @@ __device__ __forceinline__ void fft_pencil(double2 *b, int t, const double2 *__r
   fft_pass<L, SIGN, 0>(b, t, tw);
   if constexpr (Plan<L>::NPASS > 1) fft_pass<L, SIGN, 1>(b, t, tw);
   if constexpr (Plan<L>::NPASS > 2) fft_pass<L, SIGN, 2>(b, t, tw);
+}
+
+// ---------------------------------------------------------------- load/store-functor passes
+// The same Stockham passes with the first pass reading through `ld(e)` (e.g. straight from
+// HBM into registers: RMAX independent loads per thread) and the last pass writing through
+// `st(e, v)` (e.g. straight to HBM), so a 2-pass transform makes ONE shared-memory round
+// trip.  The last pass is thread-local in place (it reads and writes positions j + r*NS),
+// so results may be stored back into the same pencil without a barrier.
+template <int L, int PASS>
+struct PassI {
+  using P = Plan<L>;
+  static constexpr int R = P::radix(PASS), NS = P::ns(PASS), NR = L / R, J = NR / P::T;
+};
+
+template <int L, int SIGN, int PASS, class LDF>
+__device__ __forceinline__ void pass_lc(double2 *v, int t, const double2 *__restrict__ tw, LDF ld) {
+  using I = PassI<L, PASS>;
+#pragma unroll
+  for (int q = 0; q < I::J; ++q) {
+    const int j = t + q * Plan<L>::T;
+#pragma unroll
+    for (int r = 0; r < I::R; ++r) {
+      if constexpr (std::is_invocable_v<LDF, int, int>)
+        v[q * I::R + r] = ld(j + r * I::NR, q * I::R + r);     // (element, pass-0 slot)
+      else
+        v[q * I::R + r] = ld(j + r * I::NR);
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < I::J; ++q) {
+    const int j = t + q * Plan<L>::T;
+    if (I::NS > 1) {
+      const int jm = j % I::NS;
+#pragma unroll
+      for (int r = 1; r < I::R; ++r)
+        v[q * I::R + r] = cmul(v[q * I::R + r], twiddle<SIGN>(tw, jm * r * (L / (I::NS * I::R))));
+    }
+    dft_reg<I::R, SIGN>(&v[q * I::R]);
+  }
+}
+
+template <int L, int PASS, class STF>
+__device__ __forceinline__ void pass_st(const double2 *v, int t, STF st) {
+  using I = PassI<L, PASS>;
+#pragma unroll
+  for (int q = 0; q < I::J; ++q) {
+    const int j = t + q * Plan<L>::T;
+    const int base = (j / I::NS) * I::NS * I::R + (j % I::NS);
+#pragma unroll
+    for (int r = 0; r < I::R; ++r) st(base + r * I::NS, v[q * I::R + r]);
+  }
+}
+
+// Length-L transform of one pencil by its T threads: pass 0 reads via ld, the last pass
+// writes via st, intermediate passes exchange through the padded smem pencil sp.
+// LD_SMEM: ld reads sp itself (a barrier then separates pass-0 loads from stores).
+// WARP: the pencil's T threads are consecutive lanes of one warp (T <= 32, thread index
+// t-fastest), so exchanges need only __syncwarp; otherwise every thread of the CTA must
+// call this (it contains __syncthreads when NPASS > 1).
+template <bool WARP>
+__device__ __forceinline__ void pencil_sync() {
+  if (WARP) __syncwarp(); else __syncthreads();
+}
+
+struct NoOp {
+  __device__ __forceinline__ void operator()() const {}
+};
+
+template <int L, int SIGN, bool LD_SMEM, bool WARP, class LDF, class STF, class AF = NoOp>
+__device__ __forceinline__ void fft_io(double2 *sp, int t, const double2 *__restrict__ tw,
+                                       LDF ld, STF st, AF after_load = AF()) {
+  using P = Plan<L>;
+  static_assert(!WARP || (P::T <= 32), "pencil must fit in a warp");
+  double2 v[P::RMAX];
+  auto sst = [sp](int e, double2 x) { sp[PAD(e)] = x; };
+  auto sld = [sp](int e) { return sp[PAD(e)]; };
+  pass_lc<L, SIGN, 0>(v, t, tw, ld);
+  after_load();      // pass-0 inputs are in registers: e.g. start the next tile's prefetch
+  if constexpr (P::NPASS == 1) {
+    if (LD_SMEM) pencil_sync<WARP>();
+    pass_st<L, 0>(v, t, st);
+  } else {
+    if (LD_SMEM) pencil_sync<WARP>();
+    pass_st<L, 0>(v, t, sst);
+    pencil_sync<WARP>();
+    pass_lc<L, SIGN, 1>(v, t, tw, sld);
+    if constexpr (P::NPASS == 2) {
+      pass_st<L, 1>(v, t, st);
+    } else {
+      pencil_sync<WARP>();
+      pass_st<L, 1>(v, t, sst);
+      pencil_sync<WARP>();
+      pass_lc<L, SIGN, 2>(v, t, tw, sld);
+      pass_st<L, 2>(v, t, st);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- async prefetch (cp.async)
+// A thread copies the RMAX pass-0 inputs of its NEXT tile into thread-private shared slots
+// (slot s of thread tid at pf[s * nthreads + tid]: conflict-free), so HBM loads stay in
+// flight while the current tile is transformed.  src-size 0 zero-fills masked elements.
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem, bool pred) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  const int sz = pred ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(sz)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+template <int K>   // wait until at most K committed groups are still pending
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(K) : "memory"); }
+
+#ifndef IBK_PFD
+#define IBK_PFD 2
+#endif
+constexpr int PF_DEPTH = IBK_PFD;     // tiles in flight per thread (prefetch depth)
+
+// slot of pass-0 element e for thread t (e = t + q*T + r*NR0  ->  slot q*R0 + r)
+template <int L>
+__device__ __forceinline__ int pass0_slot(int e, int t) {
+  using I = PassI<L, 0>;
+  return ((e % I::NR - t) / Plan<L>::T) * I::R + e / I::NR;
+}
+// call f(slot, e) for the pass-0 elements of thread t
+template <int L, class F>
+__device__ __forceinline__ void pass0_foreach(int t, F f) {
+  using I = PassI<L, 0>;
+#pragma unroll
+  for (int q = 0; q < I::J; ++q)
+#pragma unroll
+    for (int r = 0; r < I::R; ++r) f(q * I::R + r, t + q * Plan<L>::T + r * I::NR);
 }
 
 }  // namespace ibk

@@ -25,15 +25,24 @@ template <int N> struct XCfg {      // x passes: RB rows of one z-plane per CTA
   static constexpr int T = Plan<M>::T;
   static constexpr int RB = (64 / T) < N ? (64 / T) : N;
 };
-template <int N> struct YCfg {      // y pass: C consecutive kx columns per CTA
-  static constexpr int T = Plan<N>::T;
-  static constexpr int C0 = 128 / T;
-  static constexpr int C = C0 < 8 ? 8 : (C0 > 32 ? 32 : C0);
+#ifndef IBK_YC
+#define IBK_YC 8
+#endif
+template <int N> struct YCfg {      // y pass: C consecutive kx columns per CTA (256-byte rows
+  static constexpr int T = Plan<N>::T;   // on the large-pitch side, see tools/membench.cu)
+  static constexpr int C = IBK_YC;
 };
+#ifndef IBK_ZC
+#define IBK_ZC 2
+#endif
+#ifndef IBK_ZMINB
+#define IBK_ZMINB 4
+#endif
 template <int N> struct ZCfg {      // z pass: C consecutive kx columns x 3 components per CTA
   static constexpr int T = Plan<N>::T;
-  static constexpr int C0 = 128 / T;
-  static constexpr int C = C0 < 4 ? 4 : (C0 > 32 ? 32 : C0);
+  static constexpr int C0 = (16 * IBK_ZC) / T;
+  static constexpr int C = C0 < 1 ? 1 : (C0 > 32 ? 32 : C0);
+  static constexpr int MINB = IBK_ZMINB;                    // CTAs/SM the registers must allow
 };
 
 __device__ __forceinline__ long long step_of(const long long *dev_n, long long n) {
@@ -70,80 +79,106 @@ cudaError_t init_tables(ib_ctx *c) {
 }
 
 // ------------------------------------------------------------------ x forward
-// MODE 0: step (r from u, F; zero F; FFT); 1: r only -> r_out; 2: FFT of `in` (1 comp).
+// MODE 0: step (r from u, F; F re-zeroed; R2C-x); 1: r only -> r_out; 2: R2C-x of `in`.
+// Thread (pencil = comp*RB + row, t): t fastest, so a warp's accesses along x are
+// contiguous.  The CTA first copies rows y0-1 .. y0+RB of plane z (3 components) to
+// shared memory with cp.async; each thread then computes r at the 2*RMAX cells of its
+// first-pass elements (z_e = r_2e + i r_2e+1) from that tile plus the z +- 1 rows (L2),
+// straight into registers.  The tile is then reused as the FFT exchange buffer.
 template <int N, int MODE>
 __global__ void __launch_bounds__(3 * XCfg<N>::RB * XCfg<N>::T)
-k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, const double *__restrict__ in,
-       double *r_out, double2 *spec, const double2 *__restrict__ twN,
-       const double2 *__restrict__ twM) {
+k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
+       const double *__restrict__ in, double *r_out, double2 *spec,
+       const double2 *__restrict__ twN, const double2 *__restrict__ twM) {
   constexpr int M = N / 2, RB = XCfg<N>::RB, T = XCfg<N>::T, LD = Plan<M>::LD;
-  constexpr int NC = MODE == 2 ? 1 : 3;
+  constexpr int NC = MODE == 2 ? 1 : 3, UR = RB + 2;
   extern __shared__ double2 sm[];
+  double *ut = reinterpret_cast<double *>(sm);     // u tile [comp][UR][N]
   const int z = blockIdx.y, y0 = blockIdx.x * RB;
+  const int t = threadIdx.x % T, pencil = threadIdx.x / T;
+  const int row = pencil % RB, comp = pencil / RB, y = y0 + row;
   const size_t V = (size_t)N * N * N;
+  const size_t rowbase = ((size_t)z * N + y) * N;
   const double cu = g.rho / g.dt, ra = g.rho * g.invh;
+  if (MODE != 2) {
+    constexpr int CH = N / 2;                      // 16-byte chunks per row
+    for (int idx = threadIdx.x; idx < 3 * UR * CH; idx += blockDim.x) {
+      const int ch = idx % CH, rr = (idx / CH) % UR, cc = idx / (CH * UR);
+      const int yy = (y0 - 1 + rr + N) & (N - 1);
+      cp_async16(ut + ((size_t)cc * UR + rr) * N + 2 * ch,
+                 u + cc * V + ((size_t)z * N + yy) * N + 2 * ch, true);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  // F is only read on rows the spread touched (row flags), else taken as 0
+  const bool hasF = MODE == 1 || (MODE == 0 && (rowflag == nullptr || rowflag[(size_t)z * N + y] != 0));
+  const size_t zm = ((size_t)((z + N - 1) & (N - 1)) * N + y) * N;
+  const size_t zp = ((size_t)((z + 1) & (N - 1)) * N + y) * N;
+  const double *uc_ = u + (MODE == 2 ? 0 : comp * V);
+  const double *own = ut + ((size_t)comp * UR + row + 1) * N;        // this row, own comp
 
-  for (int idx = threadIdx.x; idx < RB * N; idx += blockDim.x) {
-    const int row = idx / N, x = idx % N, y = y0 + row;
-    const size_t c0 = ((size_t)z * N + y) * N + x;
-    double r[3];
-    if (MODE == 2) {
-      r[0] = in[c0];
-    } else {
-      const size_t nm[3] = {((size_t)z * N + y) * N + ((x + N - 1) & (N - 1)),
-                            ((size_t)z * N + ((y + N - 1) & (N - 1))) * N + x,
-                            ((size_t)((z + N - 1) & (N - 1)) * N + y) * N + x};
-      const size_t np_[3] = {((size_t)z * N + y) * N + ((x + 1) & (N - 1)),
-                             ((size_t)z * N + ((y + 1) & (N - 1))) * N + x,
-                             ((size_t)((z + 1) & (N - 1)) * N + y) * N + x};
-      double uc[3];
-#pragma unroll
-      for (int k = 0; k < 3; ++k) uc[k] = __ldg(&u[k * V + c0]);
-#pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        const double *ui = u + i * V;
-        double adv = 0.0;
-#pragma unroll
-        for (int k = 0; k < 3; ++k) {
-          // u_k D_k^- if u_k > 0, u_k D_k^+ if u_k < 0 (backward at u_k = 0, Z5)
-          const double d = uc[k] < 0.0 ? (__ldg(&ui[np_[k]]) - uc[i]) : (uc[i] - __ldg(&ui[nm[k]]));
-          adv += uc[k] * d;
-        }
-        double Fi = F[i * V + c0];
-        r[i] = cu * uc[i] - ra * adv + Fi;
-        if (MODE == 0 && Fi != 0.0) F[i * V + c0] = 0.0;
-      }
-    }
-    if (MODE == 1) {
-#pragma unroll
-      for (int i = 0; i < 3; ++i) r_out[i * V + c0] = r[i];
-    } else {
-#pragma unroll
-      for (int i = 0; i < NC; ++i) {
-        double *p = reinterpret_cast<double *>(sm + (i * RB + row) * LD + PAD(x >> 1));
-        p[x & 1] = r[i];
-      }
-    }
+  // r at the cell pair (2e, 2e+1) of this thread's component: sum_k u_k D_k^{+-} u_i
+  // with the backward difference for u_k > 0 (and u_k = 0, Z5), the forward one for
+  // u_k < 0 (PAPER.md 676-691); all operands loaded unconditionally.
+  auto rhs2 = [&](int e) -> double2 {
+    const int x = 2 * e;
+    const double2 v0 = *reinterpret_cast<const double2 *>(ut + (0 * UR + row + 1) * N + x);
+    const double2 v1 = *reinterpret_cast<const double2 *>(ut + (1 * UR + row + 1) * N + x);
+    const double2 v2 = *reinterpret_cast<const double2 *>(ut + (2 * UR + row + 1) * N + x);
+    const double2 c = comp == 0 ? v0 : (comp == 1 ? v1 : v2);
+    const double xm = own[(x + N - 1) & (N - 1)];
+    const double xp = own[(x + 2) & (N - 1)];
+    const double2 a_ym = *reinterpret_cast<const double2 *>(own - N + x);
+    const double2 a_yp = *reinterpret_cast<const double2 *>(own + N + x);
+    const double2 a_zm = __ldg(reinterpret_cast<const double2 *>(uc_ + zm + x));
+    const double2 a_zp = __ldg(reinterpret_cast<const double2 *>(uc_ + zp + x));
+    double2 Fi = make_double2(0.0, 0.0);
+    double2 *Fp = reinterpret_cast<double2 *>(F + comp * V + rowbase + x);
+    if (hasF) Fi = *Fp;
+    const double dx0 = v0.x < 0.0 ? c.y - c.x : c.x - xm;
+    const double dx1 = v0.y < 0.0 ? xp - c.y : c.y - c.x;
+    const double dy0 = v1.x < 0.0 ? a_yp.x - c.x : c.x - a_ym.x;
+    const double dy1 = v1.y < 0.0 ? a_yp.y - c.y : c.y - a_ym.y;
+    const double dz0 = v2.x < 0.0 ? a_zp.x - c.x : c.x - a_zm.x;
+    const double dz1 = v2.y < 0.0 ? a_zp.y - c.y : c.y - a_zm.y;
+    const double adv0 = v0.x * dx0 + v1.x * dy0 + v2.x * dz0;
+    const double adv1 = v0.y * dx1 + v1.y * dy1 + v2.y * dz1;
+    if (MODE == 0 && hasF && (Fi.x != 0.0 || Fi.y != 0.0)) *Fp = make_double2(0.0, 0.0);
+    return make_double2(cu * c.x - ra * adv0 + Fi.x, cu * c.y - ra * adv1 + Fi.y);
+  };
+
+  double2 rr[Plan<M>::RMAX];
+  pass0_foreach<M>(t, [&](int slot, int e) {
+    rr[slot] = MODE == 2 ? __ldg(reinterpret_cast<const double2 *>(in + rowbase) + e) : rhs2(e);
+  });
+  if (MODE == 1) {      // r only (debug)
+    pass0_foreach<M>(t, [&](int slot, int e) {
+      reinterpret_cast<double2 *>(r_out + comp * V + rowbase)[e] = rr[slot];
+    });
+    return;
   }
-  if (MODE == 1) return;
+  auto ld = [&](int e, int slot) { return rr[slot]; };
+  double2 *sp = sm + pencil * LD;
+  auto sst = [sp](int e, double2 v) { sp[PAD(e)] = v; };
+  auto bar = []() { __syncthreads(); };             // u tile dead before pencils alias it
+  fft_io<M, -1, false, true>(sp, t, twM, ld, sst, bar);
   __syncthreads();
-  {
-    const int pencil = threadIdx.x / T, t = threadIdx.x % T;
-    fft_pencil<M, -1>(sm + pencil * LD, t, twM);
-  }
+  if (MODE == 0 && rowflag && threadIdx.x < RB) rowflag[(size_t)z * N + y0 + threadIdx.x] = 0u;
   // split the length-M transform Z of z_n = r_2n + i r_2n+1 into X_k, k = 0..M:
   // E = (Z_k + conj Z_{M-k})/2, O = -i (Z_k - conj Z_{M-k})/2, X_k = E + w^k O,
   // X_{M-k} = conj(E - w^k O), w = exp(-2 pi i/N).
   constexpr int H = M / 2 + 1;
   for (int idx = threadIdx.x; idx < NC * RB * H; idx += blockDim.x) {
-    const int pencil = idx / H, k = idx % H;
-    const int comp = pencil / RB, row = pencil % RB;
-    const double2 Zk = sm[pencil * LD + PAD(k)];
-    const double2 Zm = sm[pencil * LD + PAD((M - k) & (M - 1))];
+    const int pc = idx / H, k = idx % H;
+    const int cp = pc / RB, rw = pc % RB;
+    const double2 Zk = sm[pc * LD + PAD(k)];
+    const double2 Zm = sm[pc * LD + PAD((M - k) & (M - 1))];
     const double2 E = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
     const double2 O = make_double2(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
     const double2 wO = cmul(__ldg(&twN[k]), O);
-    double2 *out = spec + (((size_t)comp * N + z) * N + (y0 + row)) * g.P;
+    double2 *out = spec + (((size_t)cp * N + z) * N + (y0 + rw)) * g.P;
     out[k] = cadd(E, wO);
     if (k != M - k) out[M - k] = cconj(csub(E, wO));
   }
@@ -151,53 +186,107 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, const double *__res
 
 template <int N>
 static cudaError_t launch_xfwd_n(const FluidGeom &g, int mode, const double *u, double *F,
-                                 const double *in, double *r_out, double2 *spec, int ncomp,
-                                 const double2 *twN, const double2 *twM, cudaStream_t s) {
+                                 unsigned *rowflag, const double *in, double *r_out,
+                                 double2 *spec, const double2 *twN, const double2 *twM,
+                                 cudaStream_t s) {
   using X = XCfg<N>;
   dim3 grid(N / X::RB, N);
   const int nc = mode == 2 ? 1 : 3;
-  const size_t smem = (size_t)nc * X::RB * Plan<N / 2>::LD * sizeof(double2);
+  const size_t fft = (size_t)nc * X::RB * Plan<N / 2>::LD * sizeof(double2);
+  const size_t tile = mode == 2 ? 0 : (size_t)3 * (X::RB + 2) * N * sizeof(double);
+  const size_t smem = fft > tile ? fft : tile;
   const int threads = nc * X::RB * X::T;
-  (void)ncomp;
   if (mode == 0)
-    k_xfwd<N, 0><<<grid, threads, smem, s>>>(g, u, F, in, r_out, spec, twN, twM);
+    k_xfwd<N, 0><<<grid, threads, smem, s>>>(g, u, F, rowflag, in, r_out, spec, twN, twM);
   else if (mode == 1)
-    k_xfwd<N, 1><<<grid, threads, 0, s>>>(g, u, F, in, r_out, spec, twN, twM);
+    k_xfwd<N, 1><<<grid, threads, smem, s>>>(g, u, F, nullptr, in, r_out, spec, twN, twM);
   else
-    k_xfwd<N, 2><<<grid, threads, smem, s>>>(g, u, F, in, r_out, spec, twN, twM);
+    k_xfwd<N, 2><<<grid, threads, smem, s>>>(g, u, F, nullptr, in, r_out, spec, twN, twM);
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ y pass
+// Spectrum layouts (complex elements, row pitch P):
+//   S1 [comp][z][y][kx]  (x passes):   z stride N*P, y stride P
+//   S2 [comp][ky][z][kx] (z pass):     z stride P,   ky stride N*P
+// The forward y pass reads S1 and writes S2, the inverse reads S2 and writes S1, so the
+// z pass streams contiguous (ky, comp) slabs; the y passes take the large-pitch side with
+// 256-byte row segments (C = 16 columns), which tools/membench.cu measured at ~6.5 TB/s.
+// Persistent CTAs walk the (kx-block, z, comp) tiles; thread (col, t), col fastest.  Each
+// thread cp.async-prefetches the pass-0 inputs of its next tile into private smem slots
+// right after loading the current ones, so HBM loads overlap the transform.
 template <int N, int SIGN>
 __global__ void __launch_bounds__(YCfg<N>::C * YCfg<N>::T)
-k_ypass(FluidGeom g, double2 *spec, const double2 *__restrict__ twN) {
-  constexpr int C = YCfg<N>::C, T = YCfg<N>::T, LD = Plan<N>::LD, M = N / 2;
+k_ypass(FluidGeom g, const double2 *in, double2 *out, size_t in_zs, size_t in_es,
+        size_t out_zs, size_t out_es, int ncomp, const double2 *__restrict__ twN) {
+  constexpr int C = YCfg<N>::C, LD = Plan<N>::LD, M = N / 2, NT = C * Plan<N>::T;
   extern __shared__ double2 sm[];
-  const int col0 = blockIdx.x * C, z = blockIdx.y, comp = blockIdx.z;
-  double2 *base = spec + ((size_t)comp * N + z) * N * g.P;
-  for (int idx = threadIdx.x; idx < C * N; idx += blockDim.x) {
-    const int y = idx / C, col = idx % C, kx = col0 + col;
-    sm[col * LD + PAD(y)] = kx <= M ? base[(size_t)y * g.P + kx] : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  fft_pencil<N, SIGN>(sm + (threadIdx.x / T) * LD, threadIdx.x % T, twN);
-  for (int idx = threadIdx.x; idx < C * N; idx += blockDim.x) {
-    const int y = idx / C, col = idx % C, kx = col0 + col;
-    if (kx <= M) base[(size_t)y * g.P + kx] = sm[col * LD + PAD(y)];
+  double2 *pf = sm + C * LD;              // prefetch slots [PF_DEPTH][RMAX][NT]
+  constexpr int SLOTS = Plan<N>::RMAX * NT;
+  const int col = threadIdx.x % C, t = threadIdx.x / C;
+  constexpr int NBLK = (M + 1 + C - 1) / C;
+  const int ntiles = NBLK * N * ncomp;
+  const size_t cstride = (size_t)N * N * g.P;
+  auto prefetch = [&](int tile, int stage) {
+    if (tile < ntiles) {
+      const int kx = (tile % NBLK) * C + col, z = (tile / NBLK) % N, comp = tile / (NBLK * N);
+      const bool ok = kx <= M;
+      const double2 *ib = in + comp * cstride + z * in_zs + (ok ? kx : 0);
+      double2 *dst = pf + stage * SLOTS + threadIdx.x;
+      pass0_foreach<N>(t, [&](int slot, int e) { cp_async16(dst + slot * NT, ib + e * in_es, ok); });
+    }
+    cp_async_commit();                   // (possibly empty) group per tile keeps the count
+  };
+#pragma unroll
+  for (int d = 0; d < PF_DEPTH; ++d) prefetch(blockIdx.x + d * gridDim.x, d);
+  int stage = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int kx = (tile % NBLK) * C + col, z = (tile / NBLK) % N, comp = tile / (NBLK * N);
+    const bool ok = kx <= M;
+    double2 *ob = out + comp * cstride + z * out_zs + kx;
+    cp_async_wait<PF_DEPTH - 1>();
+    const double2 *src = pf + stage * SLOTS + threadIdx.x;
+    auto ld = [&](int e, int slot) { return src[slot * NT]; };
+    auto st = [&](int e, double2 v) { if (ok) ob[e * out_es] = v; };
+    auto nxt = [&]() { prefetch(tile + PF_DEPTH * gridDim.x, stage); };
+    fft_io<N, SIGN, false, false>(sm + col * LD, t, twN, ld, st, nxt);
+    stage = stage + 1 == PF_DEPTH ? 0 : stage + 1;
+    __syncthreads();                               // exchange pencils reused by next tile
   }
 }
 
+template <class K>
+static int persistent_grid(K kernel, int threads, size_t smem, int ntiles) {
+  static int nsm = 0;
+  if (!nsm) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  }
+  int per = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+  if (per < 1) per = 1;
+  return ntiles < per * nsm ? ntiles : per * nsm;
+}
+
 template <int N>
-static cudaError_t launch_ypass_n(const FluidGeom &g, int sign, double2 *spec, int ncomp,
-                                  const double2 *twN, cudaStream_t s) {
+static cudaError_t launch_ypass_n(const FluidGeom &g, int sign, const double2 *in, int in_layout,
+                                  double2 *out, int out_layout, int ncomp, const double2 *twN,
+                                  cudaStream_t s) {
   using Y = YCfg<N>;
-  dim3 grid((N / 2 + 1 + Y::C - 1) / Y::C, N, ncomp);
-  const size_t smem = (size_t)Y::C * Plan<N>::LD * sizeof(double2);
-  if (sign < 0)
-    k_ypass<N, -1><<<grid, Y::C * Y::T, smem, s>>>(g, spec, twN);
-  else
-    k_ypass<N, +1><<<grid, Y::C * Y::T, smem, s>>>(g, spec, twN);
+  const int threads = Y::C * Y::T;
+  const size_t smem = ((size_t)Y::C * Plan<N>::LD + (size_t)PF_DEPTH * Plan<N>::RMAX * threads) * sizeof(double2);
+  const int ntiles = ((N / 2 + 1 + Y::C - 1) / Y::C) * N * ncomp;
+  const size_t P = g.P, NP = (size_t)N * g.P;
+  const size_t izs = in_layout == 1 ? NP : P, ies = in_layout == 1 ? P : NP;
+  const size_t ozs = out_layout == 1 ? NP : P, oes = out_layout == 1 ? P : NP;
+  if (sign < 0) {
+    const int grid = persistent_grid(k_ypass<N, -1>, threads, smem, ntiles);
+    k_ypass<N, -1><<<grid, threads, smem, s>>>(g, in, out, izs, ies, ozs, oes, ncomp, twN);
+  } else {
+    const int grid = persistent_grid(k_ypass<N, +1>, threads, smem, ntiles);
+    k_ypass<N, +1><<<grid, threads, smem, s>>>(g, in, out, izs, ies, ozs, oes, ncomp, twN);
+  }
   return cudaGetLastError();
 }
 
@@ -205,67 +294,93 @@ static cudaError_t launch_ypass_n(const FluidGeom &g, int sign, double2 *spec, i
 // Per mode k (DESIGN.md §2 S3c):  d = rho/dt + mu (l(kx) + l(ky) + l(kz)),
 //   u^ = (r^ - s (s.r^)/|s|^2) / (d N^3),   p^ = -i (s.r^)/|s|^2 / N^3,
 //   and on the 8 null modes (every k_a in {0, N/2}): u^ = r^/(d N^3), p^ = 0.
+// Thread (t, col, group), t fastest (a quarter-warp is 8 jobs of one pencil, which the
+// PAD swizzle keeps conflict-free); groups 0..2 = velocity components, 3 = pressure.
+// Forward FFT: HBM -> registers -> smem exchange -> natural-order modes in smem; solve
+// in smem; inverse FFT: smem -> registers -> smem exchange -> HBM.
 template <int N, int MODE, bool PRESS>
-__global__ void __launch_bounds__((PRESS ? 4 : 3) * ZCfg<N>::C * ZCfg<N>::T)
+__global__ void __launch_bounds__((PRESS ? 4 : 3) * ZCfg<N>::C * ZCfg<N>::T, PRESS ? 1 : ZCfg<N>::MINB)
 k_zpass(FluidGeom g, double2 *spec, double2 *pspec, const double2 *__restrict__ twN,
         const double *__restrict__ sym_s, const double *__restrict__ sym_l) {
   constexpr int C = ZCfg<N>::C, T = ZCfg<N>::T, LD = Plan<N>::LD, M = N / 2;
+  constexpr int NG = PRESS ? 4 : 3, NT = NG * C * T;
+  constexpr int NBLK = (M + 1 + C - 1) / C;
   extern __shared__ double2 sm[];
-  const int col0 = blockIdx.x * C, ky = blockIdx.y;
-  const size_t cstride = (size_t)N * N * g.P, zstride = (size_t)N * g.P;
-  double2 *base = spec + (size_t)ky * g.P;
-  for (int idx = threadIdx.x; idx < 3 * C * N; idx += blockDim.x) {
-    const int comp = idx / (C * N), rem = idx % (C * N);
-    const int zz = rem / C, col = rem % C, kx = col0 + col;
-    sm[(comp * C + col) * LD + PAD(zz)] =
-        kx <= M ? base[comp * cstride + zz * zstride + kx] : make_double2(0.0, 0.0);
-  }
-  __syncthreads();
-  const int pencil = threadIdx.x / T, t = threadIdx.x % T;
-  fft_pencil<N, -1>(sm + pencil * LD, t, twN);
-  if (MODE == 0) {
-    const double sy = sym_s[ky], ly = sym_l[ky];
-    const bool ny = (ky == 0) || (ky == M);
-    const double invV = 1.0 / ((double)N * (double)N * (double)N);
-    for (int idx = threadIdx.x; idx < C * N; idx += blockDim.x) {
-      const int col = idx / N, kz = idx % N, kx = col0 + col;
-      if (kx > M) continue;
-      const double sx = sym_s[kx], sz = sym_s[kz];
-      const double d = g.rho / g.dt + g.mu * (sym_l[kx] + ly + sym_l[kz]);
-      const double inv = invV / d;
-      double2 *q0 = sm + (0 * C + col) * LD + PAD(kz);
-      double2 *q1 = sm + (1 * C + col) * LD + PAD(kz);
-      double2 *q2 = sm + (2 * C + col) * LD + PAD(kz);
-      const double2 r0 = *q0, r1 = *q1, r2 = *q2;
-      const bool nul = ny && (kx == 0 || kx == M) && (kz == 0 || kz == M);
-      if (nul) {
-        *q0 = cscale(r0, inv); *q1 = cscale(r1, inv); *q2 = cscale(r2, inv);
-        if (PRESS) sm[(3 * C + col) * LD + PAD(kz)] = make_double2(0.0, 0.0);
-      } else {
-        const double s2 = sx * sx + sy * sy + sz * sz;
-        const double2 sr = make_double2(sx * r0.x + sy * r1.x + sz * r2.x,
-                                        sx * r0.y + sy * r1.y + sz * r2.y);
-        const double2 q = make_double2(sr.x / s2, sr.y / s2);
-        *q0 = make_double2((r0.x - sx * q.x) * inv, (r0.y - sx * q.y) * inv);
-        *q1 = make_double2((r1.x - sy * q.x) * inv, (r1.y - sy * q.y) * inv);
-        *q2 = make_double2((r2.x - sz * q.x) * inv, (r2.y - sz * q.y) * inv);
-        if (PRESS) sm[(3 * C + col) * LD + PAD(kz)] = make_double2(q.y * invV, -q.x * invV);
+  double2 *pf = sm + NG * C * LD;         // prefetch slots [PF_DEPTH][RMAX][NT]
+  constexpr int SLOTS = Plan<N>::RMAX * NT;
+  const int t = threadIdx.x % T, col = (threadIdx.x / T) % C, grp = threadIdx.x / (C * T);
+  const int ntiles = NBLK * N;
+  const size_t zs = g.P;                           // S2 layout: [comp][ky][z][kx]
+  double2 *sp = sm + (grp * C + col) * LD;
+  auto prefetch = [&](int tile, int stage) {
+    if (tile < ntiles) {
+      const int kx = (tile % NBLK) * C + col, ky = tile / NBLK;
+      const bool ok = kx <= M && grp < 3;
+      const double2 *b = spec + ((size_t)(grp < 3 ? grp : 0) * N + ky) * N * g.P + (ok ? kx : 0);
+      double2 *dst = pf + stage * SLOTS + threadIdx.x;
+      pass0_foreach<N>(t, [&](int slot, int e) { cp_async16(dst + slot * NT, b + e * zs, ok); });
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int d = 0; d < PF_DEPTH; ++d) prefetch(blockIdx.x + d * gridDim.x, d);
+  int stage = 0;
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int col0 = (tile % NBLK) * C, ky = tile / NBLK, kx = col0 + col;
+    const bool ok = kx <= M;
+    double2 *base = grp < 3 ? spec + ((size_t)grp * N + ky) * N * g.P + kx
+                            : pspec + (size_t)ky * N * g.P + kx;
+    auto gst = [&](int e, double2 v) { if (ok) base[e * zs] = v; };
+    auto sst = [sp](int e, double2 v) { sp[PAD(e)] = v; };
+    auto sld = [sp](int e) { return sp[PAD(e)]; };
+    cp_async_wait<PF_DEPTH - 1>();
+    const int cur = stage;
+    stage = stage + 1 == PF_DEPTH ? 0 : stage + 1;
+    const double2 *src = pf + cur * SLOTS + threadIdx.x;
+    auto ld = [&](int e, int slot) { return src[slot * NT]; };
+    auto nxt = [&]() { prefetch(tile + PF_DEPTH * gridDim.x, cur); };
+    if (MODE == 1) {     // forward only (debug entry point)
+      fft_io<N, -1, false, true>(sp, t, twN, ld, gst, nxt);
+      __syncwarp();
+      continue;
+    }
+    fft_io<N, -1, false, true>(sp, t, twN, ld, sst, nxt);
+    __syncthreads();
+    {
+      const double sy = sym_s[ky], ly = sym_l[ky];
+      const bool ny = (ky == 0) || (ky == M);
+      const double invV = 1.0 / ((double)N * (double)N * (double)N);
+      for (int idx = threadIdx.x; idx < C * N; idx += blockDim.x) {
+        const int c = idx / N, kz = idx % N, kxx = col0 + c;
+        if (kxx > M) continue;
+        const double sx = sym_s[kxx], sz = sym_s[kz];
+        const double d = g.rho / g.dt + g.mu * (sym_l[kxx] + ly + sym_l[kz]);
+        double2 *q0 = sm + (0 * C + c) * LD + PAD(kz);
+        double2 *q1 = q0 + C * LD;
+        double2 *q2 = q1 + C * LD;
+        const double2 r0 = *q0, r1 = *q1, r2 = *q2;
+        const bool nul = ny && (kxx == 0 || kxx == M) && (kz == 0 || kz == M);
+        if (nul) {
+          const double inv = invV / d;
+          *q0 = cscale(r0, inv); *q1 = cscale(r1, inv); *q2 = cscale(r2, inv);
+          if (PRESS) q2[C * LD] = make_double2(0.0, 0.0);
+        } else {
+          // one division: w = 1/(d |s|^2) gives 1/d = w |s|^2 and 1/|s|^2 = w d
+          const double s2 = sx * sx + sy * sy + sz * sz;
+          const double w = 1.0 / (d * s2);
+          const double is2 = w * d, inv = invV * (w * s2);
+          const double2 q = make_double2((sx * r0.x + sy * r1.x + sz * r2.x) * is2,
+                                         (sx * r0.y + sy * r1.y + sz * r2.y) * is2);
+          *q0 = make_double2((r0.x - sx * q.x) * inv, (r0.y - sx * q.y) * inv);
+          *q1 = make_double2((r1.x - sy * q.x) * inv, (r1.y - sy * q.y) * inv);
+          *q2 = make_double2((r2.x - sz * q.x) * inv, (r2.y - sz * q.y) * inv);
+          if (PRESS) q2[C * LD] = make_double2(q.y * invV, -q.x * invV);
+        }
       }
     }
     __syncthreads();
-    fft_pencil<N, +1>(sm + pencil * LD, t, twN);
-  }
-  for (int idx = threadIdx.x; idx < 3 * C * N; idx += blockDim.x) {
-    const int comp = idx / (C * N), rem = idx % (C * N);
-    const int zz = rem / C, col = rem % C, kx = col0 + col;
-    if (kx <= M) base[comp * cstride + zz * zstride + kx] = sm[(comp * C + col) * LD + PAD(zz)];
-  }
-  if (PRESS) {
-    double2 *pb = pspec + (size_t)ky * g.P;
-    for (int idx = threadIdx.x; idx < C * N; idx += blockDim.x) {
-      const int zz = idx / C, col = idx % C, kx = col0 + col;
-      if (kx <= M) pb[zz * zstride + kx] = sm[(3 * C + col) * LD + PAD(zz)];
-    }
+    fft_io<N, +1, true, true>(sp, t, twN, sld, gst);
+    __syncwarp();                                  // pencil reused by the next tile
   }
 }
 
@@ -274,62 +389,57 @@ static cudaError_t launch_zpass_n(const FluidGeom &g, int mode, double2 *spec, d
                                   const double2 *twN, const double *s_, const double *l_,
                                   cudaStream_t s) {
   using Z = ZCfg<N>;
-  dim3 grid((N / 2 + 1 + Z::C - 1) / Z::C, N);
-  const size_t smem3 = (size_t)3 * Z::C * Plan<N>::LD * sizeof(double2);
-  const size_t smem4 = (size_t)4 * Z::C * Plan<N>::LD * sizeof(double2);
-  if (mode == 1)
-    k_zpass<N, 1, false><<<grid, 3 * Z::C * Z::T, smem3, s>>>(g, spec, pspec, twN, s_, l_);
-  else if (pspec)
-    k_zpass<N, 0, true><<<grid, 4 * Z::C * Z::T, smem4, s>>>(g, spec, pspec, twN, s_, l_);
-  else
-    k_zpass<N, 0, false><<<grid, 3 * Z::C * Z::T, smem3, s>>>(g, spec, pspec, twN, s_, l_);
+  const int ntiles = ((N / 2 + 1 + Z::C - 1) / Z::C) * N;
+  const int t3 = 3 * Z::C * Z::T, t4 = 4 * Z::C * Z::T;
+  const size_t smem3 = ((size_t)3 * Z::C * Plan<N>::LD + (size_t)PF_DEPTH * Plan<N>::RMAX * t3) * sizeof(double2);
+  const size_t smem4 = ((size_t)4 * Z::C * Plan<N>::LD + (size_t)PF_DEPTH * Plan<N>::RMAX * t4) * sizeof(double2);
+  if (mode == 1) {
+    const int grid = persistent_grid(k_zpass<N, 1, false>, t3, smem3, ntiles);
+    k_zpass<N, 1, false><<<grid, t3, smem3, s>>>(g, spec, pspec, twN, s_, l_);
+  } else if (pspec) {
+    const int grid = persistent_grid(k_zpass<N, 0, true>, t4, smem4, ntiles);
+    k_zpass<N, 0, true><<<grid, t4, smem4, s>>>(g, spec, pspec, twN, s_, l_);
+  } else {
+    const int grid = persistent_grid(k_zpass<N, 0, false>, t3, smem3, ntiles);
+    k_zpass<N, 0, false><<<grid, t3, smem3, s>>>(g, spec, pspec, twN, s_, l_);
+  }
   return cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ x inverse (C2R)
-// From X_k (k = 0..M) rebuild Z'_k = A + i c B, Z'_{M-k} = conj(A - i c B) with
-// A = X_k + conj X_{M-k}, B = X_k - conj X_{M-k}, c = exp(+2 pi i k/N); then the inverse
-// length-M FFT of Z' is N (r_even + i r_odd).
+// Z'_e = A + i c B with A = X_e + conj X_{M-e}, B = X_e - conj X_{M-e}, c = exp(+2 pi i e/N)
+// is formed while loading (both X read from HBM/L1); the inverse length-M FFT of Z' is
+// N (r_even + i r_odd), written straight from the last pass as (r_2k, r_2k+1) pairs.
 template <int N>
 __global__ void __launch_bounds__(3 * XCfg<N>::RB * XCfg<N>::T)
 k_xinv(FluidGeom g, const double2 *__restrict__ spec, double *out, int ncomp,
        const double2 *__restrict__ twN, const double2 *__restrict__ twM, long long *flag,
        const long long *dev_n, long long n) {
   constexpr int M = N / 2, RB = XCfg<N>::RB, T = XCfg<N>::T, LD = Plan<M>::LD;
-  constexpr int H = M / 2 + 1;
   extern __shared__ double2 sm[];
   const int z = blockIdx.y, y0 = blockIdx.x * RB;
-  for (int idx = threadIdx.x; idx < ncomp * RB * H; idx += blockDim.x) {
-    const int pencil = idx / H, k = idx % H;
-    const int comp = pencil / RB, row = pencil % RB;
-    const double2 *in = spec + (((size_t)comp * N + z) * N + (y0 + row)) * g.P;
-    double2 Xk = in[k], Xm = in[M - k];
-    if (k == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real
+  const int t = threadIdx.x % T, pencil = threadIdx.x / T;
+  const int row = pencil % RB, comp = pencil / RB;
+  const double2 *in = spec + (((size_t)comp * N + z) * N + (y0 + row)) * g.P;
+  const size_t V = (size_t)N * N * N;
+  double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * N + (y0 + row)) * N);
+  auto ld = [&](int e) -> double2 {
+    double2 Xk = in[e], Xm = in[M - e];
+    if (e == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real
     const double2 A = make_double2(Xk.x + Xm.x, Xk.y - Xm.y);
     const double2 B = make_double2(Xk.x - Xm.x, Xk.y + Xm.y);
-    const double2 cB = cmul(cconj(__ldg(&twN[k])), B);
-    const double2 icB = make_double2(-cB.y, cB.x);
-    sm[pencil * LD + PAD(k)] = cadd(A, icB);
-    if (k != 0 && k != M - k) sm[pencil * LD + PAD(M - k)] = cconj(csub(A, icB));
-  }
-  __syncthreads();
-  {  // blockDim = ncomp * RB * T: every thread owns a pencil (launcher guarantees)
-    const int pencil = threadIdx.x / T, t = threadIdx.x % T;
-    fft_pencil<M, +1>(sm + pencil * LD, t, twM);
-  }
+    const double2 cB = cmul(cconj(__ldg(&twN[e])), B);
+    return make_double2(A.x - cB.y, A.y + cB.x);
+  };
   bool bad = false;
-  const size_t V = (size_t)N * N * N;
-  for (int idx = threadIdx.x; idx < ncomp * RB * N; idx += blockDim.x) {
-    const int pencil = idx / N, x = idx % N;
-    const int comp = pencil / RB, row = pencil % RB;
-    const double2 v = sm[pencil * LD + PAD(x >> 1)];
-    const double val = (x & 1) ? v.y : v.x;
-    bad |= !isfinite(val);
-    out[comp * V + ((size_t)z * N + (y0 + row)) * N + x] = val;
-  }
+  auto st = [&](int k, double2 v) {
+    bad |= !(isfinite(v.x) && isfinite(v.y));
+    o2[k] = v;
+  };
+  fft_io<M, +1, false, true>(sm + pencil * LD, t, twM, ld, st);
   if (flag && __syncthreads_or(bad) && threadIdx.x == 0) {
-    const long long st = dev_n ? *dev_n - 1 : n;
-    atomicMin(flag, st);
+    const long long s = dev_n ? *dev_n - 1 : n;
+    atomicMin(flag, s);
   }
 }
 
@@ -360,16 +470,17 @@ static cudaError_t launch_xinv_n(const FluidGeom &g, const double2 *spec, double
   }
 
 cudaError_t launch_xfwd(const FluidGeom &g, int mode, const double *u, double *F,
-                        const double *in, double *r_out, double2 *spec, int ncomp,
+                        unsigned *rowflag, const double *in, double *r_out, double2 *spec,
                         const double2 *twN, const double2 *twM, cudaStream_t s) {
-#define CALL(n) launch_xfwd_n<n>(g, mode, u, F, in, r_out, spec, ncomp, twN, twM, s)
+#define CALL(n) launch_xfwd_n<n>(g, mode, u, F, rowflag, in, r_out, spec, twN, twM, s)
   IBK_DISPATCH_N(g.N, CALL)
 #undef CALL
 }
 
-cudaError_t launch_ypass(const FluidGeom &g, int sign, double2 *spec, int ncomp,
-                         const double2 *twN, cudaStream_t s) {
-#define CALL(n) launch_ypass_n<n>(g, sign, spec, ncomp, twN, s)
+cudaError_t launch_ypass(const FluidGeom &g, int sign, const double2 *in, int in_layout,
+                         double2 *out, int out_layout, int ncomp, const double2 *twN,
+                         cudaStream_t s) {
+#define CALL(n) launch_ypass_n<n>(g, sign, in, in_layout, out, out_layout, ncomp, twN, s)
   IBK_DISPATCH_N(g.N, CALL)
 #undef CALL
 }
@@ -395,7 +506,7 @@ static cudaError_t set_attrs_n() {
   const int big = 200 * 1024;
   cudaError_t e = cudaSuccess;
 #define SETA(K) if (e == cudaSuccess) e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, big)
-  SETA((k_xfwd<N, 0>)); SETA((k_xfwd<N, 2>));
+  SETA((k_xfwd<N, 0>)); SETA((k_xfwd<N, 1>)); SETA((k_xfwd<N, 2>));
   SETA((k_ypass<N, -1>)); SETA((k_ypass<N, +1>));
   SETA((k_zpass<N, 0, false>)); SETA((k_zpass<N, 0, true>)); SETA((k_zpass<N, 1, false>));
   SETA(k_xinv<N>);

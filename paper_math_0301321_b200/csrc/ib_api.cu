@@ -107,16 +107,16 @@ cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long 
   cudaError_t e;
   auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], s); };
   mark(0);
-  if ((e = launch_force_spread(sd, g, nullptr, dev_n, n, c->F, s)) != cudaSuccess) return e;
+  if ((e = launch_force_spread(sd, g, nullptr, dev_n, n, c->F, c->rowflag, s)) != cudaSuccess) return e;
   mark(1);
-  if ((e = launch_xfwd(g, 0, c->u, c->F, nullptr, nullptr, c->spec, 3, c->twN, c->twM, s)) != cudaSuccess) return e;
+  if ((e = launch_xfwd(g, 0, c->u, c->F, c->rowflag, nullptr, nullptr, c->spec, c->twN, c->twM, s)) != cudaSuccess) return e;
   mark(2);
-  if ((e = launch_ypass(g, -1, c->spec, 3, c->twN, s)) != cudaSuccess) return e;
+  if ((e = launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 3, c->twN, s)) != cudaSuccess) return e;
   mark(3);
-  if ((e = launch_zpass(g, 0, c->spec, pressure ? c->pspec : nullptr, c->twN, c->sym_s,
+  if ((e = launch_zpass(g, 0, c->spec2, pressure ? c->pspec : nullptr, c->twN, c->sym_s,
                         c->sym_l, s)) != cudaSuccess) return e;
   mark(4);
-  if ((e = launch_ypass(g, +1, c->spec, 3, c->twN, s)) != cudaSuccess) return e;
+  if ((e = launch_ypass(g, +1, c->spec2, 2, c->spec, 1, 3, c->twN, s)) != cudaSuccess) return e;
   mark(5);
   if ((e = launch_xinv(g, c->spec, c->u, 3, c->twN, c->twM, c->flag, dev_n, n, s)) != cudaSuccess) return e;
   mark(6);
@@ -169,6 +169,9 @@ ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
   if ((e = dalloc(&c->u, 3 * V)) != cudaSuccess) return bad(e, "u");
   if ((e = dalloc(&c->F, 3 * V)) != cudaSuccess) return bad(e, "F");
   if ((e = dalloc(&c->spec, S)) != cudaSuccess) return bad(e, "spectrum");
+  if ((e = dalloc(&c->spec2, S)) != cudaSuccess) return bad(e, "spectrum");
+  if ((e = dalloc(&c->rowflag, (size_t)N * N)) != cudaSuccess) return bad(e, "row flags");
+  if ((e = cudaMemsetAsync(c->rowflag, 0, (size_t)N * N * sizeof(unsigned), c->stream)) != cudaSuccess) return bad(e, "memset");
   if ((e = dalloc(&c->twN, N)) != cudaSuccess) return bad(e, "tables");
   if ((e = dalloc(&c->twM, N / 2)) != cudaSuccess) return bad(e, "tables");
   if ((e = dalloc(&c->sym_s, N)) != cudaSuccess) return bad(e, "tables");
@@ -190,7 +193,7 @@ void ib_destroy(ib_ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_graph(c);
-  dfree(c->u); dfree(c->F); dfree(c->spec); dfree(c->pspec); dfree(c->p);
+  dfree(c->u); dfree(c->F); dfree(c->rowflag); dfree(c->spec); dfree(c->spec2); dfree(c->pspec); dfree(c->pspec1); dfree(c->p);
   dfree(c->twN); dfree(c->twM); dfree(c->sym_s); dfree(c->sym_l);
   dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->drive_idx); dfree(c->drive_dir);
   dfree(c->flag); dfree(c->dev_n);
@@ -216,6 +219,7 @@ int ib_set_option(ib_ctx *c, int32_t opt, int64_t value) {
       c->want_p = value != 0;
       if (c->want_p && !c->pspec) {
         CK(dalloc(&c->pspec, (size_t)c->g.N * c->g.N * c->g.P));
+        CK(dalloc(&c->pspec1, (size_t)c->g.N * c->g.N * c->g.P));
         CK(dalloc(&c->p, (size_t)c->g.V));
       }
       return IB_OK;
@@ -402,11 +406,10 @@ int ib_get_fields(ib_ctx *c, double *u, double *p) {
   if (u) CK(copy_sync(u, c->u, (size_t)3 * c->g.V * sizeof(double), c->stream));
   if (p) {
     if (!c->have_p || !c->pspec) return fail(IB_ESTATE, "pressure not available: enable IB_OPT_PRESSURE before ib_step");
-    CK(launch_ypass(c->g, +1, c->pspec, 1, c->twN, c->stream));
-    CK(launch_xinv(c->g, c->pspec, c->p, 1, c->twN, c->twM, nullptr, nullptr, 0, c->stream));
+    CK(launch_ypass(c->g, +1, c->pspec, 2, c->pspec1, 1, 1, c->twN, c->stream));
+    CK(launch_xinv(c->g, c->pspec1, c->p, 1, c->twN, c->twM, nullptr, nullptr, 0, c->stream));
     c->launches += 2;
     CK(copy_sync(p, c->p, (size_t)c->g.V * sizeof(double), c->stream));
-    c->have_p = false;    // pspec was transformed in place
   }
   return IB_OK;
 }
@@ -476,7 +479,7 @@ int ib_debug_spread(ib_ctx *c, const double *f_node, double *F_out) {
   if (c->np > 0) {
     CK(t.get(&f, (size_t)c->np * 3));
     CK(copy_sync(f, f_node, (size_t)c->np * 3 * sizeof(double), c->stream));
-    CK(launch_force_spread(struct_dev(c), c->g, f, nullptr, c->n, F, c->stream));
+    CK(launch_force_spread(struct_dev(c), c->g, f, nullptr, c->n, F, nullptr, c->stream));
   }
   CK(copy_sync(F_out, F, 3 * V * sizeof(double), c->stream));
   return IB_OK;
@@ -502,29 +505,32 @@ int ib_debug_rhs(ib_ctx *c, const double *u, const double *F, double *r_out) {
   CK(t.get(&ud, 3 * V)); CK(t.get(&Fd, 3 * V)); CK(t.get(&r, 3 * V));
   CK(copy_sync(ud, u, 3 * V * sizeof(double), c->stream));
   CK(copy_sync(Fd, F, 3 * V * sizeof(double), c->stream));
-  CK(launch_xfwd(c->g, 1, ud, Fd, nullptr, r, c->spec, 3, c->twN, c->twM, c->stream));
+  CK(launch_xfwd(c->g, 1, ud, Fd, nullptr, nullptr, r, c->spec, c->twN, c->twM, c->stream));
   CK(copy_sync(r_out, r, 3 * V * sizeof(double), c->stream));
   return IB_OK;
 }
 
 int ib_debug_fluid(ib_ctx *c, const double *u, const double *F, double *u_out, double *p_out) {
   if (!c || !u || !F || !u_out) return fail(IB_EINVAL, "NULL argument");
-  Tmp t; double *ud, *Fd, *pd = nullptr; double2 *ps = nullptr;
+  Tmp t; double *ud, *Fd, *pd = nullptr; double2 *ps = nullptr, *ps1 = nullptr;
   const FluidGeom &g = c->g;
   const size_t V = (size_t)g.V;
   cudaStream_t s = c->stream;
   CK(t.get(&ud, 3 * V)); CK(t.get(&Fd, 3 * V));
-  if (p_out) { CK(t.get(&ps, (size_t)g.N * g.N * g.P)); CK(t.get(&pd, V)); }
+  if (p_out) {
+    CK(t.get(&ps, (size_t)g.N * g.N * g.P)); CK(t.get(&ps1, (size_t)g.N * g.N * g.P));
+    CK(t.get(&pd, V));
+  }
   CK(copy_sync(ud, u, 3 * V * sizeof(double), s));
   CK(copy_sync(Fd, F, 3 * V * sizeof(double), s));
-  CK(launch_xfwd(g, 0, ud, Fd, nullptr, nullptr, c->spec, 3, c->twN, c->twM, s));
-  CK(launch_ypass(g, -1, c->spec, 3, c->twN, s));
-  CK(launch_zpass(g, 0, c->spec, ps, c->twN, c->sym_s, c->sym_l, s));
-  CK(launch_ypass(g, +1, c->spec, 3, c->twN, s));
+  CK(launch_xfwd(g, 0, ud, Fd, nullptr, nullptr, nullptr, c->spec, c->twN, c->twM, s));
+  CK(launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 3, c->twN, s));
+  CK(launch_zpass(g, 0, c->spec2, ps, c->twN, c->sym_s, c->sym_l, s));
+  CK(launch_ypass(g, +1, c->spec2, 2, c->spec, 1, 3, c->twN, s));
   CK(launch_xinv(g, c->spec, ud, 3, c->twN, c->twM, nullptr, nullptr, 0, s));
   if (p_out) {
-    CK(launch_ypass(g, +1, ps, 1, c->twN, s));
-    CK(launch_xinv(g, ps, pd, 1, c->twN, c->twM, nullptr, nullptr, 0, s));
+    CK(launch_ypass(g, +1, ps, 2, ps1, 1, 1, c->twN, s));
+    CK(launch_xinv(g, ps1, pd, 1, c->twN, c->twM, nullptr, nullptr, 0, s));
     CK(copy_sync(p_out, pd, V * sizeof(double), s));
   }
   CK(copy_sync(u_out, ud, 3 * V * sizeof(double), s));
@@ -539,12 +545,14 @@ int ib_debug_fft(ib_ctx *c, const double *in, double *out) {
   cudaStream_t s = c->stream;
   CK(t.get(&ind, V));
   CK(copy_sync(ind, in, V * sizeof(double), s));
-  CK(launch_xfwd(g, 2, nullptr, nullptr, ind, nullptr, c->spec, 1, c->twN, c->twM, s));
-  CK(launch_ypass(g, -1, c->spec, 1, c->twN, s));
-  CK(launch_zpass(g, 1, c->spec, nullptr, c->twN, c->sym_s, c->sym_l, s));
-  CK(cudaMemcpy2DAsync(out, (size_t)(g.M + 1) * 2 * sizeof(double), c->spec,
-                       (size_t)g.P * sizeof(double2), (size_t)(g.M + 1) * sizeof(double2),
-                       (size_t)g.N * g.N, cudaMemcpyDefault, s));
+  CK(launch_xfwd(g, 2, nullptr, nullptr, nullptr, ind, nullptr, c->spec, c->twN, c->twM, s));
+  CK(launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 1, c->twN, s));
+  CK(launch_zpass(g, 1, c->spec2, nullptr, c->twN, c->sym_s, c->sym_l, s));
+  // S2 [ky][kz][kx] -> out [kz][ky][kx]
+  for (int ky = 0; ky < g.N; ++ky)
+    CK(cudaMemcpy2DAsync(out + (size_t)ky * (g.M + 1) * 2, (size_t)g.N * (g.M + 1) * 2 * sizeof(double),
+                         c->spec2 + (size_t)ky * g.N * g.P, (size_t)g.P * sizeof(double2),
+                         (size_t)(g.M + 1) * sizeof(double2), (size_t)g.N, cudaMemcpyDefault, s));
   CK(cudaStreamSynchronize(s));
   return IB_OK;
 }

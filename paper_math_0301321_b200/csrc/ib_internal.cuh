@@ -43,8 +43,11 @@ struct ib_ctx {
   // Eulerian state and work arrays
   double *u = nullptr;          // [3][V]
   double *F = nullptr;          // [3][V]  (kept zero between steps)
-  double2 *spec = nullptr;      // [3][N][N][P]
-  double2 *pspec = nullptr;     // [N][N][P]  (pressure, lazily)
+  unsigned *rowflag = nullptr;  // [N*N]: row (z,y) of F touched by the spread
+  double2 *spec = nullptr;      // S1 [3][z][y][P]  (x passes)
+  double2 *spec2 = nullptr;     // S2 [3][ky][z][P] (z pass)
+  double2 *pspec = nullptr;     // pressure, S2 layout (lazily)
+  double2 *pspec1 = nullptr;    // pressure, S1 layout (lazily)
   double *p = nullptr;          // [V] pressure output cache (lazily)
   double2 *twN = nullptr, *twM = nullptr;   // exp(-2 pi i t/L) tables
   double *sym_s = nullptr, *sym_l = nullptr; // per-axis symbols
@@ -81,12 +84,16 @@ namespace ibk {
 cudaError_t init_tables(ib_ctx *c);
 cudaError_t fluid_setup_attributes(int N);
 // x pass: mode 0 = step (r from u,F; zero F), 1 = r only (write r_out), 2 = FFT of in (1 comp)
+// rowflag (may be null = read all of F): per (z,y) row, set by the spread where F != 0
 cudaError_t launch_xfwd(const FluidGeom &g, int mode, const double *u, double *F,
-                        const double *in, double *r_out, double2 *spec, int ncomp,
+                        unsigned *rowflag, const double *in, double *r_out, double2 *spec,
                         const double2 *twN, const double2 *twM, cudaStream_t s);
-cudaError_t launch_ypass(const FluidGeom &g, int sign, double2 *spec, int ncomp,
-                         const double2 *twN, cudaStream_t s);
-// z pass: mode 0 = fwd+project+inv (pressure if pspec != null), 1 = forward only
+// y pass between spectrum layouts (1 = S1 [comp][z][y][kx], 2 = S2 [comp][ky][z][kx])
+cudaError_t launch_ypass(const FluidGeom &g, int sign, const double2 *in, int in_layout,
+                         double2 *out, int out_layout, int ncomp, const double2 *twN,
+                         cudaStream_t s);
+// z pass on an S2 spectrum: mode 0 = fwd+project+inv (pressure if pspec != null, S2),
+// 1 = forward only
 cudaError_t launch_zpass(const FluidGeom &g, int mode, double2 *spec, double2 *pspec,
                          const double2 *twN, const double *sym_s, const double *sym_l,
                          cudaStream_t s);
@@ -98,7 +105,7 @@ cudaError_t launch_force(const StructDev &sd, const long long *dev_n, long long 
                          double *f_out, cudaStream_t s);
 cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g,
                                 const double *f_in, const long long *dev_n, long long n,
-                                double *F, cudaStream_t s);
+                                double *F, unsigned *rowflag, cudaStream_t s);
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
                           cudaStream_t s);

@@ -123,7 +123,7 @@ __global__ void k_drive_add(StructDev sd, const long long *dev_n, long long n, d
 
 // Spread of the drive forces (few points): one thread per point, 192 atomics.
 __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n, long long n,
-                               double *F) {
+                               double *F, unsigned *rowflag) {
   const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (d >= sd.nd) return;
   const int N = g.N;
@@ -144,6 +144,7 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
                             ((jx + e) & (N - 1));
         const double w = wx[e] * wy[b] * wz[c];
         for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], fd[k] * w);
+        if (rowflag && e == 0) rowflag[cell / N] = 1u;
       }
 }
 
@@ -153,7 +154,8 @@ constexpr int REC = 17;    // 12 weights + 3 forces, padded to an odd stride (ba
 
 template <bool FROM_ARRAY>
 __global__ void __launch_bounds__(SPREAD_THREADS)
-k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, double *F) {
+k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, double *F,
+               unsigned *rowflag) {
   __shared__ double rec[SPREAD_THREADS / 32][32][REC];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -205,6 +207,10 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
     atomicAdd(&F[e0], acc[0]);          atomicAdd(&F[e1], acc[1]);
     atomicAdd(&F[V + e0], acc[2]);      atomicAdd(&F[V + e1], acc[3]);
     atomicAdd(&F[2 * V + e0], acc[4]);  atomicAdd(&F[2 * V + e1], acc[5]);
+    if (rowflag && a == 0) {                    // mark rows (y, z0), (y, z1) of F non-zero
+      rowflag[z0 * N + y] = 1u;
+      rowflag[z1 * N + y] = 1u;
+    }
   }
 }
 
@@ -217,16 +223,16 @@ cudaError_t launch_force(const StructDev &sd, const long long *dev_n, long long 
 
 cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const double *f_in,
                                 const long long *dev_n, long long n, double *F,
-                                cudaStream_t s) {
+                                unsigned *rowflag, cudaStream_t s) {
   const unsigned blocks = (unsigned)((sd.np + SPREAD_THREADS - 1) / SPREAD_THREADS);
   if (sd.np > 0) {
     if (f_in)
-      k_force_spread<true><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F);
+      k_force_spread<true><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag);
     else
-      k_force_spread<false><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F);
+      k_force_spread<false><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag);
   }
   if (!f_in && sd.nd > 0)
-    k_drive_spread<<<(unsigned)((sd.nd + 63) / 64), 64, 0, s>>>(sd, g, dev_n, n, F);
+    k_drive_spread<<<(unsigned)((sd.nd + 63) / 64), 64, 0, s>>>(sd, g, dev_n, n, F, rowflag);
   return cudaGetLastError();
 }
 

@@ -49,7 +49,7 @@ def load(path: Optional[str] = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or _build.SO
+    path = path or os.environ.get("IB_B200_LIB") or _build.SO   # env: dev-only variant builds
     if not os.path.exists(path):
         raise ImportError(f"{path} not found: build it with __graft_entry__.build() "
                           "(the IB step has no CPU fallback)")

@@ -1,0 +1,21 @@
+"""Quick per-stage timing of one config (dev tool): python tools/stage_bench.py [config] [steps]"""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+from gen import make_config
+from paper_math_0301321_b200 import IBContext, IB_OPT_STAGE_TIMING
+k = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+steps = int(sys.argv[2]) if len(sys.argv) > 2 else 20
+cfg = make_config(k)
+c = IBContext.from_config(cfg)
+c.step(5)
+c.set_option(IB_OPT_STAGE_TIMING, 1)
+c.stage_times(reset=True)
+s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+torch.cuda.synchronize(); s.record(); c.step(steps); e.record(); torch.cuda.synchronize()
+st = c.stage_times()
+tot = s.elapsed_time(e) / steps
+maps = [l.split()[-1] for l in open("/proc/self/maps") if ".so" in l and ("libib" in l or "variants" in l)]
+print(json.dumps({"lib": sorted(set(maps)), "cfg": k, "ms_step": round(tot, 4),
+                  "stages_us": {a: round(1e3 * b / steps, 1) for a, b in st.items()}}))
