@@ -1,0 +1,344 @@
+// fluid_tma.cu — the strided FFT passes of step 3 (PAPER.md 692-695) as TMA-fed column-tile
+// kernels for N <= 256:
+//
+//   MODE_Z    : S2 -> S2   forward z FFT, per-mode implicit-viscosity + projection solve
+//               (eq:discreteNS1-2; DESIGN.md §2 S3c, readings Z6/Z22), inverse z FFT
+//   MODE_YFWD : S1 -> S2   forward y FFT (transposing [comp][z][y][kx] -> [comp][ky][z][kx])
+//   MODE_YINV : S2 -> S1   inverse y FFT (the transpose back)
+//   MODE_ZFWD : S2 -> S2   forward z FFT only (ib_debug_fft)
+//   MODE_ZINV : S2 -> S2   inverse z FFT only (the pressure spectrum written by MODE_Z)
+//
+// A tile is 8 consecutive kx columns (128 bytes per row) x N rows x 3 components.  One
+// producer warp streams tiles HBM -> smem with cp.async.bulk.tensor (SWIZZLE_128B: element
+// (row e, column c) sits at chunk c ^ (e & 7) of its 128-byte row) into a ring of STAGES
+// buffers and drains finished tiles smem -> HBM with bulk tensor stores; 3*8*T consumer
+// threads (column fastest, so the 8 lanes of every quarter-warp touch 8 distinct 16-byte
+// bank groups in every access) transform the tile IN PLACE with the Stockham passes of
+// fft.cuh (register DFT-16, barrier, store).  Loads, compute and stores of consecutive
+// tiles overlap; nothing is staged in registers across tiles.
+#include <cstdio>
+
+#include "fft.cuh"
+#include "ib_internal.cuh"
+#include "tma.cuh"
+
+namespace ibk {
+
+enum { MODE_Z = 0, MODE_YFWD = 1, MODE_YINV = 2, MODE_ZFWD = 3, MODE_ZINV = 4 };
+
+// Column tile geometry per (N, columns C); C = 8 -> 128-byte rows, SWIZZLE_128B; C = 4 ->
+// 64-byte rows, SWIZZLE_64B.  G consumer groups work on consecutive tiles independently
+// (own named barrier), so one group's barrier waits overlap another group's arithmetic.
+template <int N, int C_, int G_>
+struct CT {
+  static constexpr int C = C_, G = G_;
+  static constexpr int T = Plan<N>::T;                 // threads per pencil
+  static constexpr int NTG = 3 * C * T;                // consumer threads per group
+  static constexpr int NT = G * NTG;                   // consumer threads
+  static constexpr int NTHR = NT + 32;                 // + one producer warp
+  static constexpr int TILE = N * C;                   // complex per component
+  static constexpr uint32_t STAGE_BYTES = 3u * TILE * 16u;
+  static constexpr int STAGES = 2 * G;
+  static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
+  static_assert(NTG % 32 == 0, "named barriers need whole warps");
+  static_assert(SMEM <= 227 * 1024, "shared memory");
+};
+// which (C, G) each pass uses: the y passes touch the large-pitch side of S2 (ky stride
+// N*P*16 B), where 128-byte rows are needed for DRAM efficiency (tools/membench.cu); the
+// z passes stay on the small pitch, where 64-byte rows stream at full rate.
+template <int N, int MODE> struct ColCfg {
+  static constexpr bool ZM = MODE == MODE_Z || MODE == MODE_ZFWD || MODE == MODE_ZINV;
+  static constexpr int C = (ZM && N >= 128) ? 4 : 8;
+  static constexpr int G = (ZM && N >= 128) ? 2 : 1;
+};
+
+// Tile element (row e, column col) in 16-byte units under the TMA swizzle of the C-wide box.
+template <int C>
+__device__ __forceinline__ int swz(int e, int col) {
+  if constexpr (C == 8) return e * 8 + (col ^ (e & 7));
+  else return e * 4 + (col ^ ((e >> 1) & 3));
+}
+
+// Pass store with a per-thread pair flip: a thread with odd t writes its outputs (r, r+1)
+// in the order (r+1, r), so for NS = 1 passes the 2 pencil jobs of a quarter-warp (4-column
+// tiles) hit rows of different parity -> distinct 64-byte-swizzle bank groups.
+template <int L, int PASS, class STF>
+__device__ __forceinline__ void pass_st_flip(const double2 *v, int t, STF st) {
+  using I = PassI<L, PASS>;
+  const bool f = t & 1;
+#pragma unroll
+  for (int q = 0; q < I::J; ++q) {
+    const int j = t + q * Plan<L>::T;
+    const int base = (j / I::NS) * I::NS * I::R + (j % I::NS);
+#pragma unroll
+    for (int r = 0; r < I::R; r += 2) {
+      const double2 a = v[q * I::R + r], b = v[q * I::R + r + 1];
+      st(base + (f ? r + 1 : r) * I::NS, f ? b : a);
+      st(base + (f ? r : r + 1) * I::NS, f ? a : b);
+    }
+  }
+}
+
+// In-place length-L Stockham transform of the pencil accessed by A(e) (a double2&), by its
+// T threads; every thread of the consumer group must call it (named barrier BAR, NTG).
+template <int L, int SIGN, int C, class ACC>
+__device__ __forceinline__ void fft_inplace(ACC A, int t, const double2 *__restrict__ tw,
+                                            int bar, int ntg) {
+  double2 v[Plan<L>::RMAX];
+  auto ld = [&](int e) { return A(e); };
+  auto st = [&](int e, double2 x) { A(e) = x; };
+  pass_lc<L, SIGN, 0>(v, t, tw, ld);
+  named_bar(bar, ntg);
+  if constexpr (C == 4 && PassI<L, 0>::NS == 1 && Plan<L>::NPASS > 1) pass_st_flip<L, 0>(v, t, st);
+  else pass_st<L, 0>(v, t, st);
+  named_bar(bar, ntg);
+  if constexpr (Plan<L>::NPASS > 1) {
+    pass_lc<L, SIGN, 1>(v, t, tw, ld);
+    named_bar(bar, ntg);
+    pass_st<L, 1>(v, t, st);
+    named_bar(bar, ntg);
+  }
+  if constexpr (Plan<L>::NPASS > 2) {
+    pass_lc<L, SIGN, 2>(v, t, tw, ld);
+    named_bar(bar, ntg);
+    pass_st<L, 2>(v, t, st);
+    named_bar(bar, ntg);
+  }
+}
+
+template <int N, int MODE>
+__global__ void __launch_bounds__(CT<N, ColCfg<N, MODE>::C, ColCfg<N, MODE>::G>::NTHR, 1)
+k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
+         const __grid_constant__ CUtensorMap map_st, double2 *pspec,
+         const double2 *__restrict__ twN, const double *__restrict__ sym_s,
+         const double *__restrict__ sym_l) {
+  using K = CT<N, ColCfg<N, MODE>::C, ColCfg<N, MODE>::G>;
+  constexpr int C = K::C, G = K::G, T = K::T, NTG = K::NTG, NT = K::NT, S = K::STAGES;
+  constexpr int M = N / 2, NB = (M + 1 + C - 1) / C;
+  extern __shared__ __align__(1024) double2 smraw[];
+  __shared__ uint64_t full[S], done[S];
+  // 1024-byte aligned ring (swizzle atoms); offset arithmetic on the __shared__ array
+  // keeps every tile access an LDS/STS (a uintptr_t round trip would make them generic)
+  double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
+  const int ntiles = NB * N;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  // 2-D maps address rows (comp*N + w)*N + r; 3-D maps (x, w, comp*N + r) — see encode()
+  constexpr bool LD3 = MODE == MODE_YINV, ST3 = MODE == MODE_YFWD;
+  if (threadIdx.x >= NT) {                               // ---------------- producer warp
+    if (threadIdx.x == NT) {
+      prefetch_tmap(&map_ld);
+      prefetch_tmap(&map_st);
+      auto load = [&](int tile, int s) {
+        const int x = 2 * C * (tile % NB), w = tile / NB;
+        double2 *b = stage0 + (size_t)s * 3 * K::TILE;
+        mbar_expect_tx(&full[s], K::STAGE_BYTES);
+        for (int c = 0; c < 3; ++c) {
+          if (LD3) tma_load_3d(b + c * K::TILE, &map_ld, x, w, c * N, &full[s]);
+          else     tma_load_2d(b + c * K::TILE, &map_ld, x, (c * N + w) * N, &full[s]);
+        }
+      };
+      auto store = [&](int tile, int s) {
+        const int x = 2 * C * (tile % NB), w = tile / NB;
+        const double2 *b = stage0 + (size_t)s * 3 * K::TILE;
+        for (int c = 0; c < 3; ++c) {
+          if (ST3) tma_store_3d(&map_st, x, w, c * N, b + c * K::TILE);
+          else     tma_store_2d(&map_st, x, (c * N + w) * N, b + c * K::TILE);
+        }
+        bulk_commit();
+      };
+      int i = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i % S;
+        if (i >= S) {                                    // slot s held tile i - S
+          mbar_wait(&done[s], ((i / S) - 1) & 1);
+          store(tile - S * gridDim.x, s);
+          bulk_wait_read0();                             // smem of slot s read out
+        }
+        load(tile, s);
+      }
+      for (int k = i - S < 0 ? 0 : i - S; k < i; ++k) {  // drain the last tiles
+        const int s = k % S;
+        mbar_wait(&done[s], (k / S) & 1);
+        store(blockIdx.x + k * gridDim.x, s);
+      }
+      bulk_wait0();
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ consumers
+  const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG, bar = 1 + grp;
+  const int col = gtid % C, t = (gtid / C) % T, comp = gtid / (C * T);
+  int i = grp;
+  for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G) {
+    const int s = i % S;
+    mbar_wait(&full[s], (i / S) & 1);
+    double2 *buf = stage0 + (size_t)s * 3 * K::TILE;
+    double2 *pc = buf + comp * K::TILE;
+    auto A = [pc, col](int e) -> double2 & { return pc[swz<C>(e, col)]; };
+    if (MODE == MODE_Z) {
+      fft_inplace<N, -1, C>(A, t, twN, bar, NTG);
+      const int kx0 = C * (tile % NB), ky = tile / NB;
+      const double sy = sym_s[ky], ly = sym_l[ky];
+      const bool ny = (ky == 0) || (ky == M);
+      const double invV = 1.0 / ((double)N * (double)N * (double)N);
+      for (int idx = gtid; idx < N * C; idx += NTG) {
+        const int c = idx % C, kz = idx / C, kx = kx0 + c;
+        if (kx > M) continue;
+        double2 *q0 = buf + swz<C>(kz, c);
+        double2 *q1 = q0 + K::TILE, *q2 = q1 + K::TILE;
+        const double2 r0 = *q0, r1 = *q1, r2 = *q2;
+        const double sx = sym_s[kx], sz = sym_s[kz];
+        const double d = g.rho / g.dt + g.mu * (sym_l[kx] + ly + sym_l[kz]);
+        const bool nul = ny && (kx == 0 || kx == M) && (kz == 0 || kz == M);
+        if (nul) {                                       // reading Z6
+          const double inv = invV / d;
+          *q0 = cscale(r0, inv); *q1 = cscale(r1, inv); *q2 = cscale(r2, inv);
+          if (pspec) pspec[((size_t)ky * N + kz) * g.P + kx] = make_double2(0.0, 0.0);
+        } else {
+          // one division: w = 1/(d |s|^2) gives 1/d = w |s|^2 and 1/|s|^2 = w d
+          const double s2 = sx * sx + sy * sy + sz * sz;
+          const double w = 1.0 / (d * s2);
+          const double is2 = w * d, inv = invV * (w * s2);
+          const double2 q = make_double2((sx * r0.x + sy * r1.x + sz * r2.x) * is2,
+                                         (sx * r0.y + sy * r1.y + sz * r2.y) * is2);
+          *q0 = make_double2((r0.x - sx * q.x) * inv, (r0.y - sx * q.y) * inv);
+          *q1 = make_double2((r1.x - sy * q.x) * inv, (r1.y - sy * q.y) * inv);
+          *q2 = make_double2((r2.x - sz * q.x) * inv, (r2.y - sz * q.y) * inv);
+          if (pspec) pspec[((size_t)ky * N + kz) * g.P + kx] = make_double2(q.y * invV, -q.x * invV);
+        }
+      }
+      named_bar(bar, NTG);
+      fft_inplace<N, +1, C>(A, t, twN, bar, NTG);
+    } else {
+      fft_inplace<N, (MODE == MODE_YINV || MODE == MODE_ZINV) ? +1 : -1, C>(A, t, twN, bar, NTG);
+    }
+    fence_proxy_async();                                 // generic writes -> TMA store
+    named_bar(bar, NTG);
+    if (gtid == 0) mbar_arrive(&done[s]);
+  }
+}
+
+// ------------------------------------------------------------------ tensor maps
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// 2-D view: rows of one spectrum array, row r = (comp*N + w)*N + e; 3-D view of S2:
+// (x, z, comp*N + ky).  Inner dimension in doubles (2 per complex, N/2+1 complex valid,
+// row pitch P complex); boxes are 2C doubles (C*16 bytes) x N rows with the matching
+// swizzle (C = 8: 128 B, C = 4: 64 B).  Columns past N/2 are zero-filled on load and
+// clipped on store.
+static bool encode(CUtensorMap *m, void *base, int rank, const FluidGeom &g, int C) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  const int N = g.N;
+  cuuint64_t dims[3], strides[2];
+  cuuint32_t box[3], es[3] = {1, 1, 1};
+  dims[0] = (cuuint64_t)2 * (g.M + 1);
+  strides[0] = (cuuint64_t)g.P * 16;
+  box[0] = (cuuint32_t)(2 * C);
+  if (rank == 2) {
+    dims[1] = (cuuint64_t)3 * N * N;
+    box[1] = (cuuint32_t)N;
+  } else {
+    dims[1] = (cuuint64_t)N;                 // z
+    dims[2] = (cuuint64_t)3 * N;             // comp*N + ky
+    strides[1] = (cuuint64_t)N * g.P * 16;
+    box[1] = 1;
+    box[2] = (cuuint32_t)N;
+  }
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  C == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+static int zcols(int N) { return N >= 128 ? 4 : 8; }
+
+bool colfft_supported(int N) { return N >= 64 && N <= 256; }
+
+bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m) {
+  return colfft_supported(g.N) && encode(m, base, 2, g, zcols(g.N));
+}
+
+cudaError_t colfft_make_maps(const FluidGeom &g, double2 *spec, double2 *spec2, TmaMaps *m) {
+  m->ok = false;
+  if (!colfft_supported(g.N)) return cudaSuccess;
+  if (!encode(&m->s1_2d, spec, 2, g, 8) || !encode(&m->s2_3d, spec2, 3, g, 8) ||
+      !encode(&m->s2_2d, spec2, 2, g, zcols(g.N)))
+    return cudaErrorInvalidValue;
+  m->ok = true;
+  return cudaSuccess;
+}
+
+template <class Kern>
+static int one_per_sm_grid(Kern k, int threads, size_t smem, int ntiles) {
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, threads, smem);
+  if (per < 1) per = 1;
+  return ntiles < per * nsm ? ntiles : per * nsm;
+}
+
+template <int N, int MODE>
+static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
+                                   const CUtensorMap &st, double2 *pspec, const double2 *twN,
+                                   const double *s_, const double *l_, cudaStream_t s) {
+  using K = CT<N, ColCfg<N, MODE>::C, ColCfg<N, MODE>::G>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_colfft<N, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  constexpr int NB = (N / 2 + 1 + K::C - 1) / K::C;   // tiles per w
+  const int grid = one_per_sm_grid(k_colfft<N, MODE>, K::NTHR, K::SMEM, NB * N);
+  k_colfft<N, MODE><<<grid, K::NTHR, K::SMEM, s>>>(g, ld, st, pspec, twN, s_, l_);
+  return cudaGetLastError();
+}
+
+template <int N>
+static cudaError_t colfft_n(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
+                            const double2 *twN, const double *s_, const double *l_,
+                            cudaStream_t s) {
+  if constexpr (N >= 64 && N <= 256) {
+    if (mode == MODE_ZINV) return launch_colfft_n<N, MODE_ZINV>(g, m.s2_2d, m.s2_2d, nullptr, twN, s_, l_, s);
+    if (mode == MODE_ZFWD) return launch_colfft_n<N, MODE_ZFWD>(g, m.s2_2d, m.s2_2d, nullptr, twN, s_, l_, s);
+    if (mode == MODE_Z) return launch_colfft_n<N, MODE_Z>(g, m.s2_2d, m.s2_2d, pspec, twN, s_, l_, s);
+    if (mode == MODE_YFWD) return launch_colfft_n<N, MODE_YFWD>(g, m.s1_2d, m.s2_3d, nullptr, twN, s_, l_, s);
+    return launch_colfft_n<N, MODE_YINV>(g, m.s2_3d, m.s1_2d, nullptr, twN, s_, l_, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_colfft(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
+                          const double2 *twN, const double *sym_s, const double *sym_l,
+                          cudaStream_t s) {
+  if (!m.ok) return cudaErrorInvalidValue;
+  switch (g.N) {
+    case 64: return colfft_n<64>(g, mode, m, pspec, twN, sym_s, sym_l, s);
+    case 128: return colfft_n<128>(g, mode, m, pspec, twN, sym_s, sym_l, s);
+    case 256: return colfft_n<256>(g, mode, m, pspec, twN, sym_s, sym_l, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ibk

@@ -69,7 +69,6 @@ __global__ void k_count_nonfinite(const double *a, size_t n, unsigned long long 
   if (c) atomicAdd(cnt, c);
 }
 
-__global__ void k_set_ll(long long *p, long long v) { *p = v; }
 
 int count_nonfinite(ib_ctx *c, const double *d, size_t n, unsigned long long *out) {
   unsigned long long *cnt;
@@ -98,6 +97,54 @@ void free_graph(ib_ctx *c) {
   c->graph_key = -1;
 }
 
+// The three strided spectrum passes: TMA column kernels when available (N in [64, 256]),
+// else the cp.async pencil kernels.
+cudaError_t yfwd(ib_ctx *c, cudaStream_t s) {
+  if (c->maps.ok) return launch_colfft(c->g, 1, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s);
+  return launch_ypass(c->g, -1, c->spec, 1, c->spec2, 2, 3, c->twN, s);
+}
+cudaError_t zsolve(ib_ctx *c, double2 *pspec, cudaStream_t s) {
+  if (c->maps.ok) return launch_colfft(c->g, 0, c->maps, pspec, c->twN, c->sym_s, c->sym_l, s);
+  return launch_zpass(c->g, 0, c->spec2, pspec, c->twN, c->sym_s, c->sym_l, s);
+}
+cudaError_t yinv(ib_ctx *c, cudaStream_t s) {
+  if (c->maps.ok) return launch_colfft(c->g, 2, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s);
+  return launch_ypass(c->g, +1, c->spec2, 2, c->spec, 1, 3, c->twN, s);
+}
+
+// Pressure half-spectrum p^ written by the z solve (S2 layout) -> p [N^3] real.  With the
+// TMA passes p^ is in full (ky, kz, kx) order and ps must hold 3 component slots (the
+// inverse-z column pass transforms all three; slots 1-2 are scratch).
+cudaError_t pressure_to_real(ib_ctx *c, double2 *ps, double2 *ps1, double *out, cudaStream_t s) {
+  cudaError_t e;
+  if (c->maps.ok) {
+    TmaMaps m;
+    if (!colfft_encode_s2(c->g, ps, &m.s2_2d)) return cudaErrorInvalidValue;
+    m.ok = true;
+    if ((e = launch_colfft(c->g, 4, m, nullptr, c->twN, c->sym_s, c->sym_l, s)) != cudaSuccess) return e;
+  }
+  if ((e = launch_ypass(c->g, +1, ps, 2, ps1, 1, 1, c->twN, s)) != cudaSuccess) return e;
+  return launch_xinv(c->g, ps1, out, 1, c->twN, c->twM, nullptr, nullptr, 0, s);
+}
+
+size_t pspec_elems(const ib_ctx *c) {
+  return (size_t)(c->maps.ok ? 3 : 1) * c->g.N * c->g.N * c->g.P;
+}
+
+// x passes: the forward pass is fluid.cu's k_xfwd; the inverse uses the TMA kernel when
+// available (N in [64, 256]).
+cudaError_t xfwd(ib_ctx *c, int mode, const double *u, double *F, unsigned *rowflag,
+                 double *r_out, cudaStream_t s) {
+  if (mode == 2)
+    return launch_xfwd(c->g, 2, nullptr, nullptr, nullptr, u, nullptr, c->spec, c->twN, c->twM, s);
+  return launch_xfwd(c->g, mode, u, F, rowflag, nullptr, r_out, c->spec, c->twN, c->twM, s);
+}
+cudaError_t xinv(ib_ctx *c, double *out, const long long *dev_n, long long n, long long *flag,
+                 cudaStream_t s) {
+  if (c->xok) return launch_xinv_tma(c->g, c->smaps, out, c->twN, c->twM, flag, dev_n, n, s);
+  return launch_xinv(c->g, c->spec, out, 3, c->twN, c->twM, flag, dev_n, n, s);
+}
+
 // Enqueue one step.  dev_n != null: step index read from device memory (graph replay).
 cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long long n,
                          cudaEvent_t *ev) {
@@ -109,16 +156,15 @@ cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long 
   mark(0);
   if ((e = launch_force_spread(sd, g, nullptr, dev_n, n, c->F, c->rowflag, s)) != cudaSuccess) return e;
   mark(1);
-  if ((e = launch_xfwd(g, 0, c->u, c->F, c->rowflag, nullptr, nullptr, c->spec, c->twN, c->twM, s)) != cudaSuccess) return e;
+  if ((e = xfwd(c, 0, c->u, c->F, c->rowflag, nullptr, s)) != cudaSuccess) return e;
   mark(2);
-  if ((e = launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 3, c->twN, s)) != cudaSuccess) return e;
+  if ((e = yfwd(c, s)) != cudaSuccess) return e;
   mark(3);
-  if ((e = launch_zpass(g, 0, c->spec2, pressure ? c->pspec : nullptr, c->twN, c->sym_s,
-                        c->sym_l, s)) != cudaSuccess) return e;
+  if ((e = zsolve(c, pressure ? c->pspec : nullptr, s)) != cudaSuccess) return e;
   mark(4);
-  if ((e = launch_ypass(g, +1, c->spec2, 2, c->spec, 1, 3, c->twN, s)) != cudaSuccess) return e;
+  if ((e = yinv(c, s)) != cudaSuccess) return e;
   mark(5);
-  if ((e = launch_xinv(g, c->spec, c->u, 3, c->twN, c->twM, c->flag, dev_n, n, s)) != cudaSuccess) return e;
+  if ((e = xinv(c, c->u, dev_n, n, c->flag, s)) != cudaSuccess) return e;
   mark(6);
   if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, s)) != cudaSuccess) return e;
   mark(7);
@@ -184,6 +230,14 @@ ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
   if ((e = cudaMemsetAsync(c->u, 0, 3 * V * sizeof(double), c->stream)) != cudaSuccess) return bad(e, "memset");
   if ((e = cudaMemsetAsync(c->F, 0, 3 * V * sizeof(double), c->stream)) != cudaSuccess) return bad(e, "memset");
   if ((e = fluid_setup_attributes(N)) != cudaSuccess) return bad(e, "attributes");
+  if ((e = colfft_make_maps(c->g, c->spec, c->spec2, &c->maps)) != cudaSuccess) return bad(e, "TMA tensor maps");
+#ifndef IBK_NO_XTMA   // dev switch: the per-CTA row kernels of fluid.cu for comparison
+  if (xpass_supported(N)) {
+    if (!xpass_encode_s1(c->g, c->spec, &c->smaps))
+      return bad(cudaErrorInvalidValue, "TMA tensor maps (x passes)");
+    c->xok = true;
+  }
+#endif
   if ((e = init_tables(c)) != cudaSuccess) return bad(e, "tables");
   if ((e = cudaStreamSynchronize(c->stream)) != cudaSuccess) return bad(e, "sync");
   return c;
@@ -218,7 +272,7 @@ int ib_set_option(ib_ctx *c, int32_t opt, int64_t value) {
     case IB_OPT_PRESSURE:
       c->want_p = value != 0;
       if (c->want_p && !c->pspec) {
-        CK(dalloc(&c->pspec, (size_t)c->g.N * c->g.N * c->g.P));
+        CK(dalloc(&c->pspec, pspec_elems(c)));
         CK(dalloc(&c->pspec1, (size_t)c->g.N * c->g.N * c->g.P));
         CK(dalloc(&c->p, (size_t)c->g.V));
       }
@@ -406,9 +460,8 @@ int ib_get_fields(ib_ctx *c, double *u, double *p) {
   if (u) CK(copy_sync(u, c->u, (size_t)3 * c->g.V * sizeof(double), c->stream));
   if (p) {
     if (!c->have_p || !c->pspec) return fail(IB_ESTATE, "pressure not available: enable IB_OPT_PRESSURE before ib_step");
-    CK(launch_ypass(c->g, +1, c->pspec, 2, c->pspec1, 1, 1, c->twN, c->stream));
-    CK(launch_xinv(c->g, c->pspec1, c->p, 1, c->twN, c->twM, nullptr, nullptr, 0, c->stream));
-    c->launches += 2;
+    CK(pressure_to_real(c, c->pspec, c->pspec1, c->p, c->stream));
+    c->launches += c->maps.ok ? 3 : 2;
     CK(copy_sync(p, c->p, (size_t)c->g.V * sizeof(double), c->stream));
   }
   return IB_OK;
@@ -505,7 +558,7 @@ int ib_debug_rhs(ib_ctx *c, const double *u, const double *F, double *r_out) {
   CK(t.get(&ud, 3 * V)); CK(t.get(&Fd, 3 * V)); CK(t.get(&r, 3 * V));
   CK(copy_sync(ud, u, 3 * V * sizeof(double), c->stream));
   CK(copy_sync(Fd, F, 3 * V * sizeof(double), c->stream));
-  CK(launch_xfwd(c->g, 1, ud, Fd, nullptr, nullptr, r, c->spec, c->twN, c->twM, c->stream));
+  CK(xfwd(c, 1, ud, Fd, nullptr, r, c->stream));
   CK(copy_sync(r_out, r, 3 * V * sizeof(double), c->stream));
   return IB_OK;
 }
@@ -518,19 +571,18 @@ int ib_debug_fluid(ib_ctx *c, const double *u, const double *F, double *u_out, d
   cudaStream_t s = c->stream;
   CK(t.get(&ud, 3 * V)); CK(t.get(&Fd, 3 * V));
   if (p_out) {
-    CK(t.get(&ps, (size_t)g.N * g.N * g.P)); CK(t.get(&ps1, (size_t)g.N * g.N * g.P));
+    CK(t.get(&ps, pspec_elems(c))); CK(t.get(&ps1, (size_t)g.N * g.N * g.P));
     CK(t.get(&pd, V));
   }
   CK(copy_sync(ud, u, 3 * V * sizeof(double), s));
   CK(copy_sync(Fd, F, 3 * V * sizeof(double), s));
-  CK(launch_xfwd(g, 0, ud, Fd, nullptr, nullptr, nullptr, c->spec, c->twN, c->twM, s));
-  CK(launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 3, c->twN, s));
-  CK(launch_zpass(g, 0, c->spec2, ps, c->twN, c->sym_s, c->sym_l, s));
-  CK(launch_ypass(g, +1, c->spec2, 2, c->spec, 1, 3, c->twN, s));
-  CK(launch_xinv(g, c->spec, ud, 3, c->twN, c->twM, nullptr, nullptr, 0, s));
+  CK(xfwd(c, 0, ud, Fd, nullptr, nullptr, s));
+  CK(yfwd(c, s));
+  CK(zsolve(c, ps, s));
+  CK(yinv(c, s));
+  CK(xinv(c, ud, nullptr, 0, nullptr, s));
   if (p_out) {
-    CK(launch_ypass(g, +1, ps, 2, ps1, 1, 1, c->twN, s));
-    CK(launch_xinv(g, ps1, pd, 1, c->twN, c->twM, nullptr, nullptr, 0, s));
+    CK(pressure_to_real(c, ps, ps1, pd, s));
     CK(copy_sync(p_out, pd, V * sizeof(double), s));
   }
   CK(copy_sync(u_out, ud, 3 * V * sizeof(double), s));
@@ -545,9 +597,14 @@ int ib_debug_fft(ib_ctx *c, const double *in, double *out) {
   cudaStream_t s = c->stream;
   CK(t.get(&ind, V));
   CK(copy_sync(ind, in, V * sizeof(double), s));
-  CK(launch_xfwd(g, 2, nullptr, nullptr, nullptr, ind, nullptr, c->spec, c->twN, c->twM, s));
-  CK(launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 1, c->twN, s));
-  CK(launch_zpass(g, 1, c->spec2, nullptr, c->twN, c->sym_s, c->sym_l, s));
+  CK(xfwd(c, 2, ind, nullptr, nullptr, nullptr, s));
+  if (c->maps.ok) {      // TMA passes transform all 3 component slots (only slot 0 is read)
+    CK(launch_colfft(g, 1, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s));
+    CK(launch_colfft(g, 3, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s));
+  } else {
+    CK(launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 1, c->twN, s));
+    CK(launch_zpass(g, 1, c->spec2, nullptr, c->twN, c->sym_s, c->sym_l, s));
+  }
   // S2 [ky][kz][kx] -> out [kz][ky][kx]
   for (int ky = 0; ky < g.N; ++ky)
     CK(cudaMemcpy2DAsync(out + (size_t)ky * (g.M + 1) * 2, (size_t)g.N * (g.M + 1) * 2 * sizeof(double),

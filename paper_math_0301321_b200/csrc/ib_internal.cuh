@@ -1,5 +1,6 @@
 // ib_internal.cuh — context layout and kernel launchers of the B200 IB step.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -31,6 +32,18 @@ struct FluidGeom {
   double h, invh, rho, mu, dt;
 };
 
+// TMA descriptors of the two spectrum arrays (fluid_tma.cu), valid when ok.
+struct TmaMaps {
+  CUtensorMap s1_2d, s2_2d, s2_3d;
+  bool ok = false;
+};
+
+// TMA descriptors of the inverse x pass (xpass_tma.cu): S1 spectrum rows (kx < N/2 box and
+// the Nyquist column).
+struct XMapsS {
+  CUtensorMap main, nyq;
+};
+
 enum { STAGE_FORCE_SPREAD = 0, STAGE_XFWD, STAGE_YFWD, STAGE_ZPROJ, STAGE_YINV, STAGE_XINV,
        STAGE_INTERP, STAGE_COUNT };
 
@@ -51,6 +64,9 @@ struct ib_ctx {
   double *p = nullptr;          // [V] pressure output cache (lazily)
   double2 *twN = nullptr, *twM = nullptr;   // exp(-2 pi i t/L) tables
   double *sym_s = nullptr, *sym_l = nullptr; // per-axis symbols
+  ibk::TmaMaps maps;                         // TMA column-pass descriptors (N in [64, 256])
+  ibk::XMapsS smaps;                         // TMA x-inverse descriptors of spec
+  bool xok = false;
   // Lagrangian state
   int64_t np = 0;
   double *X = nullptr;
@@ -100,6 +116,21 @@ cudaError_t launch_zpass(const FluidGeom &g, int mode, double2 *spec, double2 *p
 cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, int ncomp,
                         const double2 *twN, const double2 *twM, long long *flag,
                         const long long *dev_n, long long n, cudaStream_t s);
+// TMA column passes (fluid_tma.cu): mode 0 = z fwd+solve+inv on S2 (pressure to pspec if
+// non-null; p^ in (ky, kz, kx) order), 1 = y fwd S1->S2, 2 = y inv S2->S1, 3 = z forward
+// only on S2, 4 = z inverse only on S2 (uses maps.s2_2d)
+bool colfft_supported(int N);
+bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m);
+cudaError_t colfft_make_maps(const FluidGeom &g, double2 *spec, double2 *spec2, TmaMaps *m);
+cudaError_t launch_colfft(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
+                          const double2 *twN, const double *sym_s, const double *sym_l,
+                          cudaStream_t s);
+// TMA inverse x pass (xpass_tma.cu), N in [64, 256]: S1 -> out (3 components)
+bool xpass_supported(int N);
+bool xpass_encode_s1(const FluidGeom &g, const double2 *spec, XMapsS *m);
+cudaError_t launch_xinv_tma(const FluidGeom &g, const XMapsS &m, double *out,
+                            const double2 *twN, const double2 *twM, long long *flag,
+                            const long long *dev_n, long long n, cudaStream_t s);
 // Lagrangian kernels (lagrangian.cu)
 cudaError_t launch_force(const StructDev &sd, const long long *dev_n, long long n,
                          double *f_out, cudaStream_t s);

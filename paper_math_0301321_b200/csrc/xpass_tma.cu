@@ -1,0 +1,211 @@
+// xpass_tma.cu — the inverse x pass of step 3 for N in [64, 256], persistent and TMA-fed:
+//
+//   k_xinv_tma : complex-to-real FFT along x of the S1 spectrum -> u^{n+1} (PAPER.md
+//                692-695), with the non-finite check of ib_step.
+//
+// A tile is RB consecutive y rows of one z plane, all 3 components.  A producer warp streams
+// tiles into a ring of STAGES shared-memory buffers with cp.async.bulk.tensor (a kx < N/2 row
+// box and the Nyquist column box); G consumer groups (own named barrier) take alternate
+// tiles.  The tile buffer is reused as the FFT exchange space once a group's pass-0 inputs
+// are in registers; results go straight to HBM with coalesced 16-byte stores, so a buffer
+// is released as soon as its tile is transformed.  (A TMA-fed forward x pass was measured
+// slower than fluid.cu's k_xfwd — its z +- 1 L2 reads need more resident warps than the
+// 10-warp, 168-register budget leaves.)
+#include <climits>
+
+#include "fft.cuh"
+#include "ib_internal.cuh"
+#include "tma.cuh"
+
+namespace ibk {
+
+template <int N>
+struct XT {
+  static constexpr int M = N / 2;
+  static constexpr int T = Plan<M>::T;                  // threads per pencil
+  // 3 groups of 3 warps + the producer = 10 warps: <= 204 registers per thread, so the
+  // FFT state never spills (spills would miss the small L1 left beside ~200 KB of smem)
+  static constexpr int RB = 32 / T < N ? 32 / T : N;    // rows per tile
+  static constexpr int NTG = 3 * RB * T;                // consumer threads per group
+  static constexpr int G = 3;
+  static constexpr int NT = G * NTG;
+  static constexpr int NTHR = NT + 32;
+  static constexpr int LD = Plan<M>::LD;
+  static constexpr size_t PENC = (size_t)3 * RB * LD * 16;          // exchange pencils
+  static constexpr int NQ = RB > 8 ? RB : 8;         // Nyquist slot stride (128-B aligned)
+  static constexpr size_t XI = (size_t)3 * RB * N * 8 + 3 * NQ * 16; // xinv S1 rows + Nyquist
+  static constexpr size_t SI = ((XI > PENC ? XI : PENC) + 1023) & ~(size_t)1023;
+  static constexpr int SI_STAGES = 6;
+  static_assert(NTG % 32 == 0, "whole warps per group");
+};
+
+// ------------------------------------------------------------------ x inverse (C2R)
+// Z'_e = A + i c B, A = X_e + conj X_{M-e}, B = X_e - conj X_{M-e}, c = exp(+2 pi i e/N)
+// (see fluid.cu k_xinv), inverse length-M FFT, (r_2k, r_2k+1) pairs straight to HBM.
+template <int N>
+__global__ void __launch_bounds__(XT<N>::NTHR, 1)
+k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
+           const __grid_constant__ CUtensorMap map_nyq, double *out,
+           const double2 *__restrict__ twN, const double2 *__restrict__ twM, long long *flag,
+           const long long *dev_n, long long n) {
+  using K = XT<N>;
+  constexpr int M = K::M, RB = K::RB, T = K::T, LD = K::LD, NTG = K::NTG, G = K::G;
+  constexpr int S = K::SI_STAGES, NYB = N / RB;
+  extern __shared__ __align__(1024) double2 smraw[];
+  __shared__ uint64_t full[S], done[S];
+  __shared__ int bad_any[G];
+  double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
+  constexpr size_t SW = K::SI / 16;
+  const int ntiles = N * NYB;
+  const size_t V = (size_t)N * N * N;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
+    fence_mbar_init();
+  }
+  if (threadIdx.x < G) bad_any[threadIdx.x] = 0;
+  __syncthreads();
+
+  if (threadIdx.x >= K::NT) {                             // -------------- producer warp
+    if (threadIdx.x == K::NT) {
+      prefetch_tmap(&map_main);
+      prefetch_tmap(&map_nyq);
+      int i = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
+        const int s = i % S;
+        if (i >= S) mbar_wait(&done[s], ((i / S) - 1) & 1);
+        const int z = tile / NYB, y0 = (tile % NYB) * RB;
+        double2 *b = stage0 + (size_t)s * SW;            // [3][RB][M] then [3][RB] Nyquist
+        mbar_expect_tx(&full[s], (uint32_t)(3 * RB * (M + 1) * 16));
+        for (int c = 0; c < 3; ++c) {
+          const int r0 = (c * N + z) * N + y0;
+          tma_load_2d(b + (size_t)c * RB * M, &map_main, 0, r0, &full[s]);
+          tma_load_2d(b + (size_t)3 * RB * M + c * K::NQ, &map_nyq, 2 * M, r0, &full[s]);
+        }
+      }
+    }
+    return;
+  }
+
+  const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG, bar = 1 + grp;
+  const int t = gtid % T, pencil = gtid / T, row = pencil % RB, comp = pencil / RB;
+  const long long step = dev_n ? *dev_n - 1 : n;
+  int i = grp;
+  bool bad = false;
+  for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G) {
+    const int s = i % S;
+    const int z = tile / NYB, y0 = (tile % NYB) * RB;
+    double2 *sm = stage0 + (size_t)s * SW;
+    const double2 *in = sm + (size_t)(comp * RB + row) * M;
+    mbar_wait(&full[s], (i / S) & 1);
+    const double2 nyq = sm[(size_t)3 * RB * M + comp * K::NQ + row];
+    double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * N + (y0 + row)) * N);
+    auto ld = [&](int e) -> double2 {
+      double2 Xk = in[e], Xm = e == 0 ? nyq : in[M - e];
+      if (e == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real
+      const double2 A = make_double2(Xk.x + Xm.x, Xk.y - Xm.y);
+      const double2 B = make_double2(Xk.x - Xm.x, Xk.y + Xm.y);
+      const double2 cB = cmul(cconj(__ldg(&twN[e])), B);
+      return make_double2(A.x - cB.y, A.y + cB.x);
+    };
+    auto st = [&](int k, double2 v) {
+      bad |= !(isfinite(v.x) && isfinite(v.y));
+      o2[k] = v;
+    };
+    // pass-0 loads read the stage (all group threads) before any pencil store aliases it
+    auto sync_after_load = [&]() { named_bar(bar, NTG); };
+    double2 *sp = sm + pencil * LD;
+    fft_io<M, +1, false, true>(sp, t, twM, ld, st, sync_after_load);
+    named_bar(bar, NTG);
+    if (gtid == 0) mbar_arrive(&done[s]);
+  }
+  if (flag && bad) bad_any[grp] = 1;
+  named_bar(1 + grp, NTG);
+  if (flag && gtid == 0 && bad_any[grp]) atomicMin(flag, step);
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_x() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                         &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+// rows x cols doubles (row pitch `pitch` bytes), box box_cols x box_rows, no swizzle
+static bool encode_rows(CUtensorMap *m, const void *base, uint64_t rows, uint64_t cols,
+                        uint64_t pitch, uint32_t box_cols, uint32_t box_rows) {
+  auto fn = encode_fn_x();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows}, strides[1] = {pitch};
+  cuuint32_t box[2] = {box_cols, box_rows}, es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<void *>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static int xt_rb(int N) {
+  switch (N) {
+    case 64: return XT<64>::RB;
+    case 128: return XT<128>::RB;
+    case 256: return XT<256>::RB;
+    default: return 0;
+  }
+}
+
+bool xpass_supported(int N) { return N >= 64 && N <= 256; }
+
+bool xpass_encode_s1(const FluidGeom &g, const double2 *spec, XMapsS *m) {
+  const int N = g.N;
+  if (!xpass_supported(N)) return false;
+  return encode_rows(&m->main, spec, (uint64_t)3 * N * N, 2 * (g.M + 1), (uint64_t)g.P * 16, N,
+                     xt_rb(N)) &&
+         encode_rows(&m->nyq, spec, (uint64_t)3 * N * N, 2 * (g.M + 1), (uint64_t)g.P * 16, 2,
+                     xt_rb(N));
+}
+
+template <class Kern>
+static int grid_for(Kern k, int threads, size_t smem, int ntiles) {
+  int dev = 0, nsm = 0, per = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, threads, smem);
+  if (per < 1) per = 1;
+  return ntiles < per * nsm ? ntiles : per * nsm;
+}
+
+template <int N>
+static cudaError_t xinv_n(const FluidGeom &g, const XMapsS &m, double *out, const double2 *twN,
+                          const double2 *twM, long long *flag, const long long *dev_n,
+                          long long n, cudaStream_t s) {
+  using K = XT<N>;
+  const size_t smem = (size_t)K::SI_STAGES * K::SI + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k_xinv_tma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  const int grid = grid_for(k_xinv_tma<N>, K::NTHR, smem, N * (N / K::RB));
+  k_xinv_tma<N><<<grid, K::NTHR, smem, s>>>(g, m.main, m.nyq, out, twN, twM, flag, dev_n, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_xinv_tma(const FluidGeom &g, const XMapsS &m, double *out,
+                            const double2 *twN, const double2 *twM, long long *flag,
+                            const long long *dev_n, long long n, cudaStream_t s) {
+  switch (g.N) {
+    case 64: return xinv_n<64>(g, m, out, twN, twM, flag, dev_n, n, s);
+    case 128: return xinv_n<128>(g, m, out, twN, twM, flag, dev_n, n, s);
+    case 256: return xinv_n<256>(g, m, out, twN, twM, flag, dev_n, n, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace ibk

@@ -9,9 +9,10 @@ import sys
 
 rep, kern = sys.argv[1], sys.argv[2]
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 25
+skip = int(sys.argv[4]) if len(sys.argv) > 4 else 0      # n-th matching launch
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--kernel-name",
-                      f"regex:{kern}", "--print-source", "sass"], capture_output=True,
-                     text=True).stdout
+                      f"regex:{kern}", "--launch-skip", str(skip), "--launch-count", "1",
+                      "--print-source", "sass"], capture_output=True, text=True).stdout
 lines = out.splitlines()
 # first line = kernel name row
 rows = list(csv.reader(io.StringIO("\n".join(lines[1:]))))
