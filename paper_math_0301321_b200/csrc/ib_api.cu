@@ -85,7 +85,7 @@ int count_nonfinite(ib_ctx *c, const double *d, size_t n, unsigned long long *ou
 
 StructDev struct_dev(const ib_ctx *c) {
   StructDev s;
-  s.X = c->X; s.np = c->np; s.patches = c->patches; s.npatch = c->npatch; s.stiff = c->stiff;
+  s.X = c->X; s.np = c->np; s.perm = c->since_bin >= 0 ? c->perm : nullptr; s.patches = c->patches; s.npatch = c->npatch; s.stiff = c->stiff;
   s.nd = c->nd; s.drive_idx = c->drive_idx; s.drive_dir = c->drive_dir;
   s.drive_amp = c->drive_amp; s.drive_period = c->drive_period;
   return s;
@@ -145,13 +145,25 @@ cudaError_t xinv(ib_ctx *c, double *out, const long long *dev_n, long long n, lo
   return launch_xinv(c->g, c->spec, out, 3, c->twN, c->twM, flag, dev_n, n, s);
 }
 
+// (Re)bin the points by base cell when the permutation is missing or SORT_PERIOD steps old.
+cudaError_t ensure_binned(ib_ctx *c, cudaStream_t s) {
+  if (c->np == 0 || (c->since_bin >= 0 && c->since_bin < SORT_PERIOD)) return cudaSuccess;
+  cudaError_t e = launch_bin(c->g, c->X, c->np, c->bincnt, c->binsum, c->perm, s);
+  if (e == cudaSuccess) {
+    c->since_bin = 0;
+    c->launches += 5;
+  }
+  return e;
+}
+
 // Enqueue one step.  dev_n != null: step index read from device memory (graph replay).
 cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long long n,
                          cudaEvent_t *ev) {
   const FluidGeom &g = c->g;
   cudaStream_t s = c->stream;
-  StructDev sd = struct_dev(c);
   cudaError_t e;
+  if ((e = ensure_binned(c, s)) != cudaSuccess) return e;
+  StructDev sd = struct_dev(c);
   auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], s); };
   mark(0);
   if ((e = launch_force_spread(sd, g, nullptr, dev_n, n, c->F, c->rowflag, s)) != cudaSuccess) return e;
@@ -166,8 +178,9 @@ cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long 
   mark(5);
   if ((e = xinv(c, c->u, dev_n, n, c->flag, s)) != cudaSuccess) return e;
   mark(6);
-  if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, s)) != cudaSuccess) return e;
+  if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, sd.perm, s)) != cudaSuccess) return e;
   mark(7);
+  c->since_bin++;
   return cudaSuccess;
 }
 
@@ -250,6 +263,7 @@ void ib_destroy(ib_ctx *c) {
   dfree(c->u); dfree(c->F); dfree(c->rowflag); dfree(c->spec); dfree(c->spec2); dfree(c->pspec); dfree(c->pspec1); dfree(c->p);
   dfree(c->twN); dfree(c->twM); dfree(c->sym_s); dfree(c->sym_l);
   dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->drive_idx); dfree(c->drive_dir);
+  dfree(c->perm); dfree(c->bincnt); dfree(c->binsum);
   dfree(c->flag); dfree(c->dev_n);
   if (c->flag_h) cudaFreeHost(c->flag_h);
   for (int k = 0; k <= STAGE_COUNT; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
@@ -342,9 +356,15 @@ int ib_set_structure(ib_ctx *c, const double *points, int64_t np, const ib_patch
   // upload
   free_graph(c);
   CK(cudaStreamSynchronize(c->stream));
-  dfree(c->X); dfree(c->patches); dfree(c->stiff);
-  c->X = nullptr; c->patches = nullptr; c->stiff = nullptr;
+  dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->perm);
+  c->X = nullptr; c->patches = nullptr; c->stiff = nullptr; c->perm = nullptr;
+  c->since_bin = -1;
   CK(dalloc(&c->X, (size_t)np * 3));
+  CK(dalloc(&c->perm, (size_t)np));
+  if (np > 0 && !c->bincnt) {
+    CK(dalloc(&c->bincnt, (size_t)c->g.V));
+    CK(dalloc(&c->binsum, (size_t)bin_scan_blocks(c->g.V)));
+  }
   CK(dalloc(&c->patches, (size_t)npatch));
   CK(dalloc(&c->stiff, (size_t)nstiff));
   CK(copy_sync(c->X, X.data(), X.size() * sizeof(double), c->stream));
@@ -361,6 +381,7 @@ int ib_set_positions(ib_ctx *c, const double *points) {
   if (c->np == 0) return IB_OK;
   if (!points) return fail(IB_EINVAL, "points is NULL");
   CK(copy_sync(c->X, points, (size_t)c->np * 3 * sizeof(double), c->stream));
+  c->since_bin = -1;
   unsigned long long bad = 0;
   int rc = count_nonfinite(c, c->X, (size_t)c->np * 3, &bad);
   if (rc) return rc;
@@ -532,6 +553,7 @@ int ib_debug_spread(ib_ctx *c, const double *f_node, double *F_out) {
   if (c->np > 0) {
     CK(t.get(&f, (size_t)c->np * 3));
     CK(copy_sync(f, f_node, (size_t)c->np * 3 * sizeof(double), c->stream));
+    CK(ensure_binned(c, c->stream));
     CK(launch_force_spread(struct_dev(c), c->g, f, nullptr, c->n, F, nullptr, c->stream));
   }
   CK(copy_sync(F_out, F, 3 * V * sizeof(double), c->stream));
@@ -546,7 +568,8 @@ int ib_debug_interp(ib_ctx *c, const double *u, double *U_out) {
   CK(t.get(&ud, 3 * V));
   CK(t.get(&U, (size_t)c->np * 3));
   CK(copy_sync(ud, u, 3 * V * sizeof(double), c->stream));
-  CK(launch_interp(c->g, ud, c->X, c->np, U, nullptr, nullptr, 0, c->stream));
+  CK(ensure_binned(c, c->stream));
+  CK(launch_interp(c->g, ud, c->X, c->np, U, nullptr, nullptr, 0, struct_dev(c).perm, c->stream));
   CK(copy_sync(U_out, U, (size_t)c->np * 3 * sizeof(double), c->stream));
   return IB_OK;
 }

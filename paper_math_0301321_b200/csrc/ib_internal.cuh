@@ -15,6 +15,7 @@ namespace ibk {
 struct StructDev {
   const double *X;            // [np][3]
   int64_t np;
+  const int *perm;            // cell-binned visiting order of the points (or null)
   const ib_patch *patches;    // [npatch]
   int32_t npatch;
   const double *stiff;
@@ -70,6 +71,9 @@ struct ib_ctx {
   // Lagrangian state
   int64_t np = 0;
   double *X = nullptr;
+  int *perm = nullptr;          // [np] cell-binned order (binning scratch: bincnt [V], binsum)
+  unsigned *bincnt = nullptr, *binsum = nullptr;
+  int64_t since_bin = -1;       // steps since the last binning (-1: perm invalid)
   ib_patch *patches = nullptr;
   int32_t npatch = 0;
   double *stiff = nullptr;
@@ -139,5 +143,10 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g,
                                 double *F, unsigned *rowflag, cudaStream_t s);
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
-                          cudaStream_t s);
+                          const int *perm, cudaStream_t s);
+// cell binning: perm = point indices grouped by base cell (5 launches + 1 memset)
+cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
+                       unsigned *bsum, int *perm, cudaStream_t s);
+int bin_scan_blocks(int64_t V);
+constexpr int SORT_PERIOD = 32;   // steps between re-binnings inside ib_step
 }  // namespace ibk

@@ -8,7 +8,9 @@
 //          shared memory, the warp's 32 lanes then own the 64 nodes x 3 components of the
 //          box (6 outputs per lane), sum the group's contributions in registers and flush
 //          once with fp64 atomicAdd — one atomic per (group, node, component) instead of
-//          one per (point, node, component).
+//          one per (point, node, component).  Points are visited in cell-binned order
+//          (a counting sort by base cell, refreshed every SORT_PERIOD steps), so a warp's
+//          lanes mostly share one box and the groups are large.
 //   interp + update (eq:discreteX, PAPER.md 725-734): gather of u^{n+1} at X^n fused with
 //          X^{n+1} = X^n + dt U, with a non-finite check.
 #include <climits>
@@ -158,13 +160,14 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
                unsigned *rowflag) {
   __shared__ double rec[SPREAD_THREADS / 32][32][REC];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int N = g.N;
   const size_t V = (size_t)g.V;
   double *r = rec[warp][lane];
   unsigned key = 0xffffffffu;
   bool live = false;
-  if (i < sd.np) {
+  if (k < sd.np) {
+    const int64_t i = sd.perm ? (int64_t)__ldg(&sd.perm[k]) : k;   // cell-binned order
     double f[3];
     if (FROM_ARRAY) {
       f[0] = __ldg(&f_in[3 * i]); f[1] = __ldg(&f_in[3 * i + 1]); f[2] = __ldg(&f_in[3 * i + 2]);
@@ -239,10 +242,13 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
 // ------------------------------------------------------------------ interp + update
 __global__ void __launch_bounds__(256)
 k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
-         long long *flag, const long long *dev_n, long long n) {
-  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+         long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   bool bad = false;
-  if (i < np) {
+  if (k < np) {
+    // cell-binned order: the lanes of a warp mostly share one 4x4x4 support box, so the
+    // 192 gathers of a warp hit the same L1 lines (broadcast)
+    const int64_t i = perm ? (int64_t)__ldg(&perm[k]) : k;
     const int N = g.N;
     const size_t V = (size_t)g.V;
     const double x0 = X[3 * i + 0], x1 = X[3 * i + 1], x2 = X[3 * i + 2];
@@ -250,23 +256,48 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
     const int jx = axis_weights(x0, g.invh, wx);
     const int jy = axis_weights(x1, g.invh, wy);
     const int jz = axis_weights(x2, g.invh, wz);
+    // U = sum_c wz_c sum_b wy_b (sum_a wx_a u(jx+a, jy+b, jz+c)): row sums first (4 FMAs
+    // per row and component), 32-bit cell offsets (3V < 2^31 for N <= 512); a row with no
+    // periodic wrap in x (the common case) is 4 consecutive doubles off one base pointer
+    int ro[4][4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        ro[c][b] = (((jz + c) & (N - 1)) * N + ((jy + b) & (N - 1))) * N;
     double U0 = 0.0, U1 = 0.0, U2 = 0.0;
+    const int Vi = (int)V;
+    if (jx >= 0 && jx + 3 < N) {
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const size_t z = (size_t)((jz + c) & (N - 1));
+      for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const size_t row = (z * N + ((jy + b) & (N - 1))) * N;
-        const double wbc = wy[b] * wz[c];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const size_t cell = row + ((jx + e) & (N - 1));
-          const double w = wx[e] * wbc;
-          U0 += __ldg(&u[cell]) * w;
-          U1 += __ldg(&u[V + cell]) * w;
-          U2 += __ldg(&u[2 * V + cell]) * w;
+        for (int b = 0; b < 4; ++b) {
+          const double *r0 = u + (ro[c][b] + jx), *r1 = r0 + Vi, *r2 = r1 + Vi;
+          const double s0 = wx[0] * __ldg(r0) + wx[1] * __ldg(r0 + 1) + wx[2] * __ldg(r0 + 2) + wx[3] * __ldg(r0 + 3);
+          const double s1 = wx[0] * __ldg(r1) + wx[1] * __ldg(r1 + 1) + wx[2] * __ldg(r1 + 2) + wx[3] * __ldg(r1 + 3);
+          const double s2 = wx[0] * __ldg(r2) + wx[1] * __ldg(r2 + 1) + wx[2] * __ldg(r2 + 2) + wx[3] * __ldg(r2 + 3);
+          const double wbc = wy[b] * wz[c];
+          U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
         }
-      }
+    } else {
+      int xo[4];
+#pragma unroll
+      for (int a = 0; a < 4; ++a) xo[a] = (jx + a) & (N - 1);
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const double *r0 = u + ro[c][b], *r1 = r0 + Vi, *r2 = r1 + Vi;
+          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            s0 += wx[a] * __ldg(r0 + xo[a]);
+            s1 += wx[a] * __ldg(r1 + xo[a]);
+            s2 += wx[a] * __ldg(r2 + xo[a]);
+          }
+          const double wbc = wy[b] * wz[c];
+          U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
+        }
     }
     if (U_out) {
       U_out[3 * i + 0] = U0; U_out[3 * i + 1] = U1; U_out[3 * i + 2] = U2;
@@ -284,10 +315,129 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
 
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
-                          cudaStream_t s) {
+                          const int *perm, cudaStream_t s) {
   if (np > 0)
-    k_interp<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(g, u, X, np, U_out, flag, dev_n, n);
+    k_interp<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(g, u, X, np, U_out, flag, dev_n, n,
+                                                          perm);
   return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ cell binning
+// perm = point indices grouped by the base cell floor(X/h) mod N of their delta support
+// (a counting sort over the N^3 cells: count, exclusive scan, scatter).  Only the order in
+// which spread/interp visit points depends on it, never a result beyond fp64 summation
+// order; ib_step refreshes it every IB_SORT_PERIOD steps.
+__device__ __forceinline__ unsigned cell_key(const double *X, int64_t i, double invh, int N) {
+  const int cx = (int)(long long)floor(X[3 * i + 0] * invh) & (N - 1);
+  const int cy = (int)(long long)floor(X[3 * i + 1] * invh) & (N - 1);
+  const int cz = (int)(long long)floor(X[3 * i + 2] * invh) & (N - 1);
+  return ((unsigned)cz * N + (unsigned)cy) * N + (unsigned)cx;
+}
+
+__global__ void k_bin_count(const double *__restrict__ X, int64_t np, double invh, int N,
+                            unsigned *cnt) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ok = i < np;
+  const unsigned key = ok ? cell_key(X, i, invh, N) : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  if (ok && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&cnt[key], __popc(peers));
+}
+
+constexpr int SCAN_T = 1024, SCAN_E = 8;          // block scan: 8192 counters per block
+
+__device__ __forceinline__ unsigned block_exclusive_scan(unsigned v, unsigned *ws, unsigned *total) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  unsigned x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) ws[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    unsigned t = ws[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const unsigned y = __shfl_up_sync(0xffffffffu, t, o);
+      if (lane >= o) t += y;
+    }
+    ws[lane] = t;                                  // inclusive warp totals
+  }
+  __syncthreads();
+  const unsigned before = (w ? ws[w - 1] : 0u) + x - v;
+  if (total) *total = ws[31];
+  __syncthreads();
+  return before;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_partial(const unsigned *cnt, size_t n, unsigned *bsum) {
+  __shared__ unsigned ws[32];
+  const size_t base = (size_t)blockIdx.x * SCAN_T * SCAN_E + (size_t)threadIdx.x * SCAN_E;
+  unsigned s = 0;
+#pragma unroll
+  for (int e = 0; e < SCAN_E; ++e) s += base + e < n ? cnt[base + e] : 0u;
+  unsigned tot;
+  block_exclusive_scan(s, ws, &tot);
+  if (threadIdx.x == 0) bsum[blockIdx.x] = tot;
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_bsum(unsigned *bsum, int nb) {
+  __shared__ unsigned ws[32];
+  unsigned carry = 0;
+  for (int b0 = 0; b0 < nb; b0 += SCAN_T) {
+    const int b = b0 + threadIdx.x;
+    const unsigned v = b < nb ? bsum[b] : 0u;
+    unsigned tot;
+    const unsigned ex = block_exclusive_scan(v, ws, &tot);
+    if (b < nb) bsum[b] = carry + ex;
+    carry += tot;
+  }
+}
+
+__global__ void __launch_bounds__(SCAN_T) k_scan_final(unsigned *cnt, size_t n, const unsigned *bsum) {
+  __shared__ unsigned ws[32];
+  const size_t base = (size_t)blockIdx.x * SCAN_T * SCAN_E + (size_t)threadIdx.x * SCAN_E;
+  unsigned v[SCAN_E], s = 0;
+#pragma unroll
+  for (int e = 0; e < SCAN_E; ++e) { v[e] = base + e < n ? cnt[base + e] : 0u; s += v[e]; }
+  unsigned run = bsum[blockIdx.x] + block_exclusive_scan(s, ws, nullptr);
+#pragma unroll
+  for (int e = 0; e < SCAN_E; ++e)
+    if (base + e < n) { cnt[base + e] = run; run += v[e]; }
+}
+
+__global__ void k_bin_scatter(const double *__restrict__ X, int64_t np, double invh, int N,
+                              unsigned *off, int *perm) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool ok = i < np;
+  const unsigned key = ok ? cell_key(X, i, invh, N) : 0xffffffffu;
+  const unsigned peers = __match_any_sync(0xffffffffu, key);
+  const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
+  unsigned base = 0;
+  if (ok && lane == leader) base = atomicAdd(&off[key], __popc(peers));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (ok) perm[base + __popc(peers & ((1u << lane) - 1u))] = (int)i;
+}
+
+cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
+                       unsigned *bsum, int *perm, cudaStream_t s) {
+  if (np <= 0) return cudaSuccess;
+  const size_t n = (size_t)g.V;
+  const int nb = (int)((n + (size_t)SCAN_T * SCAN_E - 1) / ((size_t)SCAN_T * SCAN_E));
+  const unsigned pb = (unsigned)((np + 255) / 256);
+  cudaError_t e = cudaMemsetAsync(cnt, 0, n * sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  k_bin_count<<<pb, 256, 0, s>>>(X, np, g.invh, g.N, cnt);
+  k_scan_partial<<<nb, SCAN_T, 0, s>>>(cnt, n, bsum);
+  k_scan_bsum<<<1, SCAN_T, 0, s>>>(bsum, nb);
+  k_scan_final<<<nb, SCAN_T, 0, s>>>(cnt, n, bsum);
+  k_bin_scatter<<<pb, 256, 0, s>>>(X, np, g.invh, g.N, cnt, perm);
+  return cudaGetLastError();
+}
+
+int bin_scan_blocks(int64_t V) {
+  return (int)((V + (int64_t)SCAN_T * SCAN_E - 1) / ((int64_t)SCAN_T * SCAN_E));
 }
 
 }  // namespace ibk
