@@ -74,28 +74,68 @@ def ncu_traffic(stage: str):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi sampling of SM clocks and throttle reasons during the timed region."""
+    """SM clocks and throttle reasons sampled DURING the timed region (NVML every ~10 ms,
+    nvidia-smi as a fallback), summarised as {"sm_mhz": median, "sm_max_mhz", "reasons"}."""
+    REASONS = {0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown"}
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, gpu_index: int):
+    def __init__(self, gpu_index: int, period_s: float = 0.01):
         self.idx = gpu_index
-        self.rows = []
+        self.period = period_s
+        self.sm, self.mx, self.reasons = [], [], set()
+        self.source = None
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[gpu_index]) if vis and vis.split(",")[0].isdigit() else gpu_index
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(phys)
+            self._nvml = pynvml
+            self.source = "nvml"
+        except Exception:
+            self.source = "nvidia-smi"
+
+    def _sample_nvml(self):
+        p = self._nvml
+        self.sm.append(float(p.nvmlDeviceGetClockInfo(self._h, p.NVML_CLOCK_SM)))
+        self.mx.append(float(p.nvmlDeviceGetMaxClockInfo(self._h, p.NVML_CLOCK_SM)))
+        try:
+            bits = p.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except Exception:
+            bits = p.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        for b, nm in self.REASONS.items():
+            if bits & b:
+                self.reasons.add(nm)
+
+    def _sample_smi(self):
+        out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        if not out:
+            return
+        r = [x.strip() for x in out.split(",")]
+        if r[1].replace(".", "").isdigit():
+            self.sm.append(float(r[1]))
+        if r[2].replace(".", "").isdigit():
+            self.mx.append(float(r[2]))
+        for k, nm in enumerate(["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown",
+                                "sw_power_cap"]):
+            if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
+                self.reasons.add(nm)
 
     def _run(self):
         while not self._stop.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([x.strip() for x in out.split(",")])
+                self._sample_nvml() if self._nvml else self._sample_smi()
             except Exception:
                 pass
-            self._stop.wait(0.2)
+            self._stop.wait(self.period)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
@@ -108,19 +148,11 @@ class ClockSampler:
             self._t.join(timeout=6)
 
     def summary(self) -> dict:
-        if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in self.rows:
-            for k, nm in enumerate(names):
-                if len(r) > 5 + k and r[5 + k].lower().startswith("active"):
-                    reasons.add(nm)
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+        if not self.sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"],
+                    "samples": 0, "source": self.source}
+        return {"sm_mhz": float(np.median(self.sm)), "sm_max_mhz": max(self.mx) if self.mx else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": self.source}
 
 
 # ------------------------------------------------------------------ distributed helpers
@@ -200,9 +232,8 @@ def run_ours(args, ws, rank, local):
     ctx.set_stream(stream.cuda_stream)
     with torch.cuda.stream(stream):
         ctx.step(args.warmup)                              # untimed warm-up
-        ctx.set_option(IB_OPT_STAGE_TIMING, 1)
-        ctx.stage_times(reset=True)
         ctx.launch_count(reset=True)
+        # (A) the headline: the product path (CUDA-graph replays), device-timed
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -214,6 +245,16 @@ def run_ours(args, ws, rank, local):
         barrier()
         ms = e0.elapsed_time(e1)
         launches = ctx.launch_count(reset=True)
+        # (B) per-stage CUDA events on the context stream (graph off while recording them)
+        ctx.set_option(IB_OPT_STAGE_TIMING, 1)
+        ctx.stage_times(reset=True)
+        torch.cuda.synchronize()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        ctx.step(args.steps)
+        f1.record(stream)
+        torch.cuda.synchronize()
+        ms_staged = f0.elapsed_time(f1)
         stages = ctx.stage_times(reset=True)
         ctx.set_option(IB_OPT_STAGE_TIMING, 0)
     ms_max = reduce_max(ms)
@@ -235,6 +276,9 @@ def run_ours(args, ws, rank, local):
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
             "peak_source": peaks["source"],
+            "timing": "kernel: mean per-stage CUDA-event time over a second timed region of "
+                      f"{args.steps} steps (stage events, no graph; {ms_staged / args.steps:.4f} "
+                      "ms/step there)",
             "step": {"alg_bytes": step_bytes, "ms": ms_max / args.steps,
                      "gbs": step_bytes / (ms_max / args.steps / 1e3) / 1e9,
                      "frac": step_bytes / (ms_max / args.steps / 1e3) / 1e9 / peaks["hbm_gbs"],
@@ -282,24 +326,27 @@ def run_ours(args, ws, rank, local):
 
 
 def cpu_baseline(args):
-    """The oracle as it stands, on this host's cores, on a bounded sample: 1 IB step of
-    the same config (about 10 s at 256^3 on 8 cores)."""
+    """The oracle as it stands, on this host's cores, on a bounded sample: IB steps of the
+    same config until about 10 s of CPU time have passed (at least one step)."""
     import oracle
     from gen import make_config
     oracle.set_threads(os.cpu_count() or 1)
     cfg = make_config(args.config)
     o = oracle.Oracle.from_config(cfg)
-    t0 = time.perf_counter()
-    o.step(1)
+    k, t0 = 0, time.perf_counter()
+    while k < 1 or (time.perf_counter() - t0 < 10.0 and k < 50):
+        o.step(1)
+        k += 1
     dt = time.perf_counter() - t0
-    return {"value": 1.0 / dt, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": f"1 full IB step of cfg{args.config} ({cfg.N}^3, {cfg.np_} points)"}
+    return {"value": k / dt, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+            "sample": f"{k} full IB steps of cfg{args.config} ({cfg.N}^3, {cfg.np_} points), "
+                      f"{dt:.1f} s"}
 
 
 def main(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", type=int, default=4)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")

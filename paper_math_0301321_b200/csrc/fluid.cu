@@ -438,7 +438,7 @@ k_xinv(FluidGeom g, const double2 *__restrict__ spec, double *out, int ncomp,
   };
   fft_io<M, +1, false, true>(sm + pencil * LD, t, twM, ld, st);
   if (flag && __syncthreads_or(bad) && threadIdx.x == 0) {
-    const long long s = dev_n ? *dev_n - 1 : n;
+    const long long s = dev_n ? *dev_n : n;
     atomicMin(flag, s);
   }
 }

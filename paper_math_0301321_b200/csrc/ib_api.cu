@@ -1,10 +1,11 @@
 // ib_api.cu — the C-ABI of include/ib.h: context, validation, memory, the step loop.
 //
-// One ib_step step is 6-8 launches on the context stream:
+// One ib_step step is 7-9 launches on the context stream:
 //   force+spread [+drive spread] -> xfwd (rhs + R2C-x) -> y fwd -> z fwd+solve+inv
-//   -> y inv -> xinv (C2R-x, u^{n+1}) -> interp+update (X^{n+1}).
-// Steps are optionally captured once as a CUDA graph and replayed (IB_OPT_GRAPH); the
-// step index then lives in device memory (incremented by the xfwd kernel).
+//   -> y inv -> xinv (C2R-x, u^{n+1}) -> interp+update (X^{n+1}) -> step counter + 1.
+// The step index lives in device memory, so one step is captured once as a CUDA graph and
+// replayed (IB_OPT_GRAPH, default on); the points are re-binned by cell (5 launches) outside
+// the graph every SORT_PERIOD steps.
 #include <cuda_runtime.h>
 
 #include <climits>
@@ -156,13 +157,14 @@ cudaError_t ensure_binned(ib_ctx *c, cudaStream_t s) {
   return e;
 }
 
-// Enqueue one step.  dev_n != null: step index read from device memory (graph replay).
-cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long long n,
-                         cudaEvent_t *ev) {
+// Enqueue one step (binning is the caller's job).  The step index is read on the device
+// from c->dev_n and advanced by the step's last launch, so the same sequence is captured once
+// as a CUDA graph and replayed.
+cudaError_t enqueue_step(ib_ctx *c, bool pressure, cudaEvent_t *ev) {
   const FluidGeom &g = c->g;
   cudaStream_t s = c->stream;
+  const long long *dev_n = c->dev_n, n = 0;
   cudaError_t e;
-  if ((e = ensure_binned(c, s)) != cudaSuccess) return e;
   StructDev sd = struct_dev(c);
   auto mark = [&](int k) { if (ev) cudaEventRecord(ev[k], s); };
   mark(0);
@@ -180,12 +182,28 @@ cudaError_t enqueue_step(ib_ctx *c, bool pressure, const long long *dev_n, long 
   mark(6);
   if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, sd.perm, s)) != cudaSuccess) return e;
   mark(7);
-  c->since_bin++;
-  return cudaSuccess;
+  return launch_step_inc(c->dev_n, s);
 }
 
-int64_t launches_per_step(const ib_ctx *c) {
-  return 5 + (c->np > 0 ? 2 : 0) + (c->nd > 0 && c->np >= 0 ? 1 : 0);
+int64_t launches_per_step(const ib_ctx *c, bool pressure) {
+  (void)pressure;
+  return 6 + (c->np > 0 ? 2 : 0) + (c->nd > 0 && c->np > 0 ? 1 : 0);
+}
+
+// One step as a CUDA graph (captured on first use, replayed until invalidated).
+cudaError_t graph_step(ib_ctx *c) {
+  if (!c->graph) {
+    cudaGraph_t gr = nullptr;
+    cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) return e;
+    e = enqueue_step(c, false, nullptr);
+    cudaError_t e2 = cudaStreamEndCapture(c->stream, &gr);
+    if (e == cudaSuccess) e = e2;
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->graph, gr, 0);
+    if (gr) cudaGraphDestroy(gr);
+    if (e != cudaSuccess) { c->graph = nullptr; return e; }
+  }
+  return cudaGraphLaunch(c->graph, c->stream);
 }
 
 struct Tmp {
@@ -451,10 +469,19 @@ int ib_step(ib_ctx *c, int32_t nsteps) {
       c->ev_pool.push_back(e);
     }
   }
+  const long long n0 = c->n;
+  CK(cudaMemcpyAsync(c->dev_n, &n0, sizeof(long long), cudaMemcpyHostToDevice, s));
+  CK(cudaStreamSynchronize(s));                 // n0 lives on the host stack
   for (int32_t k = 0; k < nsteps; ++k) {
     const bool pressure = c->want_p && k == nsteps - 1;
-    CK(enqueue_step(c, pressure, nullptr, c->n + k, timing ? &c->ev_pool[k * per] : nullptr));
-    c->launches += launches_per_step(c);
+    CK(ensure_binned(c, s));                    // outside the graph (it holds only pointers)
+    if (c->use_graph && !timing && !pressure) {
+      CK(graph_step(c));
+    } else {
+      CK(enqueue_step(c, pressure, timing ? &c->ev_pool[k * per] : nullptr));
+    }
+    c->since_bin++;
+    c->launches += launches_per_step(c, pressure);
   }
   CK(cudaMemcpyAsync(c->flag_h, c->flag, sizeof(long long), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

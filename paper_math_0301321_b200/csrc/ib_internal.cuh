@@ -93,10 +93,10 @@ struct ib_ctx {
   double stage_ms[ibk::STAGE_COUNT] = {};
   std::vector<cudaEvent_t> ev_pool;   // per-step stage events (IB_OPT_STAGE_TIMING)
   int64_t launches = 0;
-  // CUDA graph of one step (valid while graph_key matches)
+  // CUDA graph of one step (rebuilt after any change of structure, drive, stream, options)
   cudaGraphExec_t graph = nullptr;
   long long graph_key = -1;
-  long long *dev_n = nullptr;   // device step counter used by graph replays
+  long long *dev_n = nullptr;   // device step counter (drive phase, non-finite flag)
 };
 
 namespace ibk {
@@ -148,5 +148,6 @@ cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_
 cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
                        unsigned *bsum, int *perm, cudaStream_t s);
 int bin_scan_blocks(int64_t V);
+cudaError_t launch_step_inc(long long *dev_n, cudaStream_t s);
 constexpr int SORT_PERIOD = 32;   // steps between re-binnings inside ib_step
 }  // namespace ibk

@@ -51,20 +51,22 @@ __device__ __forceinline__ void spring(const double *__restrict__ X, double xi, 
   f[2] += t * dz;
 }
 
-__device__ __forceinline__ void point_force(const StructDev &sd, int64_t i, double f[3]) {
+// pt: the patch table (shared-memory copy when it fits, else sd.patches)
+__device__ __forceinline__ void point_force(const StructDev &sd, const ib_patch *pt, int64_t i,
+                                            double f[3]) {
   int lo = 0, hi = sd.npatch - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
-    if (__ldg(&sd.patches[mid].first) <= i) lo = mid; else hi = mid - 1;
+    if (pt[mid].first <= i) lo = mid; else hi = mid - 1;
   }
-  const ib_patch *P = sd.patches + lo;
-  const int64_t first = __ldg(&P->first);
-  const int n1 = __ldg(&P->n1), n2 = __ldg(&P->n2);
-  const uint32_t fl = __ldg(&P->flags);
+  const ib_patch *P = pt + lo;
+  const int64_t first = P->first;
+  const int n1 = P->n1, n2 = P->n2;
+  const uint32_t fl = P->flags;
   const int64_t npts = (int64_t)n1 * n2;
   const int64_t li = i - first;
   const int i1 = (int)(li % n1), i2 = (int)(li / n1);
-  const double *b = sd.stiff + __ldg(&P->param_off);
+  const double *b = sd.stiff + P->param_off;
   const double xi = __ldg(&sd.X[3 * i + 0]), yi = __ldg(&sd.X[3 * i + 1]),
                zi = __ldg(&sd.X[3 * i + 2]);
   f[0] = f[1] = f[2] = 0.0;
@@ -109,7 +111,7 @@ __global__ void k_force(StructDev sd, const long long *dev_n, long long n, doubl
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= sd.np) return;
   double f[3];
-  point_force(sd, i, f);
+  point_force(sd, sd.patches, i, f);
   f_out[3 * i + 0] = f[0];
   f_out[3 * i + 1] = f[1];
   f_out[3 * i + 2] = f[2];
@@ -123,10 +125,12 @@ __global__ void k_drive_add(StructDev sd, const long long *dev_n, long long n, d
   for (int c = 0; c < 3; ++c) f_out[3 * i + c] += a * sd.drive_dir[3 * d + c];
 }
 
-// Spread of the drive forces (few points): one thread per point, 192 atomics.
+// Spread of the drive forces (few points): one warp per driven point, each lane owning 2 of
+// the 64 support nodes x 3 components (6 atomics per lane).
 __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n, long long n,
                                double *F, unsigned *rowflag) {
-  const int64_t d = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
   if (d >= sd.nd) return;
   const int N = g.N;
   const size_t V = (size_t)g.V;
@@ -137,29 +141,36 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
   const int jx = axis_weights(sd.X[3 * i + 0], g.invh, wx);
   const int jy = axis_weights(sd.X[3 * i + 1], g.invh, wy);
   const int jz = axis_weights(sd.X[3 * i + 2], g.invh, wz);
-  const double fd[3] = {a * sd.drive_dir[3 * d], a * sd.drive_dir[3 * d + 1],
-                        a * sd.drive_dir[3 * d + 2]};
-  for (int c = 0; c < 4; ++c)
-    for (int b = 0; b < 4; ++b)
-      for (int e = 0; e < 4; ++e) {
-        const size_t cell = ((size_t)((jz + c) & (N - 1)) * N + ((jy + b) & (N - 1))) * N +
-                            ((jx + e) & (N - 1));
-        const double w = wx[e] * wy[b] * wz[c];
-        for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], fd[k] * w);
-        if (rowflag && e == 0) rowflag[cell / N] = 1u;
-      }
+  const int e = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
+  const size_t x = (jx + e) & (N - 1), y = (jy + b) & (N - 1);
+#pragma unroll
+  for (int h = 0; h < 2; ++h) {
+    const size_t z = (jz + c0 + 2 * h) & (N - 1);
+    const size_t cell = (z * N + y) * N + x;
+    const double w = a * wx[e] * wy[b] * wz[c0 + 2 * h];
+    for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], w * sd.drive_dir[3 * d + k]);
+    if (rowflag && e == 0) rowflag[z * N + y] = 1u;
+  }
 }
 
 // ------------------------------------------------------------------ force + spread
 constexpr int SPREAD_THREADS = 256;
 constexpr int REC = 17;    // 12 weights + 3 forces, padded to an odd stride (bank spread)
+constexpr int PTAB = 64;   // patch table entries staged in shared memory
 
 template <bool FROM_ARRAY>
 __global__ void __launch_bounds__(SPREAD_THREADS)
 k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, double *F,
                unsigned *rowflag) {
-  __shared__ double rec[SPREAD_THREADS / 32][32][REC];
+  __shared__ double rec[SPREAD_THREADS / 32][33][REC];     // record 32: zeros (unroll tail)
+  __shared__ ib_patch ptab[PTAB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const bool small = sd.npatch <= PTAB;
+  if (!FROM_ARRAY && small)
+    for (int q = threadIdx.x; q < sd.npatch; q += blockDim.x) ptab[q] = sd.patches[q];
+  if (lane < REC) rec[warp][32][lane] = 0.0;
+  __syncthreads();
+  const ib_patch *pt = small ? ptab : sd.patches;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int N = g.N;
   const size_t V = (size_t)g.V;
@@ -167,12 +178,20 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
   unsigned key = 0xffffffffu;
   bool live = false;
   if (k < sd.np) {
+#ifdef IBK_SP_NOPERM   // dev timing experiment only
+    const int64_t i = k;
+#else
     const int64_t i = sd.perm ? (int64_t)__ldg(&sd.perm[k]) : k;   // cell-binned order
+#endif
     double f[3];
     if (FROM_ARRAY) {
       f[0] = __ldg(&f_in[3 * i]); f[1] = __ldg(&f_in[3 * i + 1]); f[2] = __ldg(&f_in[3 * i + 2]);
     } else {
-      point_force(sd, i, f);
+#ifdef IBK_SP_NOFORCE   // dev timing experiment only
+      f[0] = 1e-3 * (double)(i & 7); f[1] = 1e-3; f[2] = -1e-3;
+#else
+      point_force(sd, pt, i, f);
+#endif
     }
     const double ih3 = g.invh * g.invh * g.invh;
     live = (f[0] != 0.0) || (f[1] != 0.0) || (f[2] != 0.0);
@@ -183,7 +202,12 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
     key = ((unsigned)jz * N + (unsigned)jy) * N + (unsigned)jx;
   }
   __syncwarp();
+  const int lgN = __ffs(N) - 1;          // N is a power of two: no integer division below
   unsigned todo = __ballot_sync(0xffffffffu, live);
+#ifdef IBK_SP_NOGROUPS   // dev timing experiment only
+  if (live && r[12] == 1.2345e300) F[0] = 1.0;
+  todo = 0;
+#endif
   // lane -> outputs (a, b, c0 | c0 + 2, component 0..2)
   const int a = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
   while (todo) {
@@ -193,20 +217,29 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
     todo &= ~grp;
     double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
     unsigned m = grp;
-    while (m) {
+#ifdef IBK_SP_NOLOOP   // dev timing experiment only
+    m = 0;
+#endif
+    while (m) {              // two members per iteration (record 32 = zero pads the tail)
       const int p = __ffs(m) - 1;
       m &= m - 1;
-      const double *q = rec[warp][p];
-      const double wab = q[a] * q[4 + b];
+      const int p2 = m ? __ffs(m) - 1 : 32;
+      m &= m - 1;
+      const double *q = rec[warp][p], *q2 = rec[warp][p2];
+      const double wab = q[a] * q[4 + b], wab2 = q2[a] * q2[4 + b];
       const double w0 = wab * q[8 + c0], w1 = wab * q[10 + c0];
-      acc[0] += q[12] * w0; acc[1] += q[12] * w1;
-      acc[2] += q[13] * w0; acc[3] += q[13] * w1;
-      acc[4] += q[14] * w0; acc[5] += q[14] * w1;
+      const double v0 = wab2 * q2[8 + c0], v1 = wab2 * q2[10 + c0];
+      acc[0] += q[12] * w0 + q2[12] * v0; acc[1] += q[12] * w1 + q2[12] * v1;
+      acc[2] += q[13] * w0 + q2[13] * v0; acc[3] += q[13] * w1 + q2[13] * v1;
+      acc[4] += q[14] * w0 + q2[14] * v0; acc[5] += q[14] * w1 + q2[14] * v1;
     }
-    const unsigned jx = kl % N, jy = (kl / N) % N, jz = kl / (N * N);
+    const unsigned jx = kl & (N - 1), jy = (kl >> lgN) & (N - 1), jz = kl >> (2 * lgN);
     const size_t x = (jx + a) & (N - 1), y = (jy + b) & (N - 1);
     const size_t z0 = (jz + c0) & (N - 1), z1 = (jz + c0 + 2) & (N - 1);
     const size_t e0 = (z0 * N + y) * N + x, e1 = (z1 * N + y) * N + x;
+#ifdef IBK_SP_NOFLUSH   // dev timing experiment only
+    if (acc[0] == 1.2345e300)
+#endif
     atomicAdd(&F[e0], acc[0]);          atomicAdd(&F[e1], acc[1]);
     atomicAdd(&F[V + e0], acc[2]);      atomicAdd(&F[V + e1], acc[3]);
     atomicAdd(&F[2 * V + e0], acc[4]);  atomicAdd(&F[2 * V + e1], acc[5]);
@@ -235,7 +268,7 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
       k_force_spread<false><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag);
   }
   if (!f_in && sd.nd > 0)
-    k_drive_spread<<<(unsigned)((sd.nd + 63) / 64), 64, 0, s>>>(sd, g, dev_n, n, F, rowflag);
+    k_drive_spread<<<(unsigned)((sd.nd * 32 + 127) / 128), 128, 0, s>>>(sd, g, dev_n, n, F, rowflag);
   return cudaGetLastError();
 }
 
@@ -308,7 +341,7 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
     }
   }
   if (flag && __syncthreads_or(bad) && threadIdx.x == 0) {
-    const long long st = dev_n ? *dev_n - 1 : n;
+    const long long st = dev_n ? *dev_n : n;
     atomicMin(flag, st);
   }
 }
@@ -319,6 +352,15 @@ cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_
   if (np > 0)
     k_interp<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(g, u, X, np, U_out, flag, dev_n, n,
                                                           perm);
+  return cudaGetLastError();
+}
+
+// End of a step: the device step counter read by the drive and the non-finite flag advances
+// (graph replays carry no host-side step index).
+__global__ void k_step_inc(long long *dev_n) { *dev_n += 1; }
+
+cudaError_t launch_step_inc(long long *dev_n, cudaStream_t s) {
+  k_step_inc<<<1, 1, 0, s>>>(dev_n);
   return cudaGetLastError();
 }
 

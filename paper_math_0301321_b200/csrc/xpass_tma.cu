@@ -88,7 +88,7 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
 
   const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG, bar = 1 + grp;
   const int t = gtid % T, pencil = gtid / T, row = pencil % RB, comp = pencil / RB;
-  const long long step = dev_n ? *dev_n - 1 : n;
+  const long long step = dev_n ? *dev_n : n;
   int i = grp;
   bool bad = false;
   for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G) {
