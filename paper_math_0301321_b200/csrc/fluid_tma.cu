@@ -1,5 +1,5 @@
 // fluid_tma.cu — the strided FFT passes of step 3 (PAPER.md 692-695) as TMA-fed column-tile
-// kernels for N <= 256:
+// kernels for N in [64, 512]:
 //
 //   MODE_Z    : S2 -> S2   forward z FFT, per-mode implicit-viscosity + projection solve
 //               (eq:discreteNS1-2; DESIGN.md §2 S3c, readings Z6/Z22), inverse z FFT
@@ -25,31 +25,47 @@
 namespace ibk {
 
 enum { MODE_Z = 0, MODE_YFWD = 1, MODE_YINV = 2, MODE_ZFWD = 3, MODE_ZINV = 4 };
+#ifndef IBK_YG256
+#define IBK_YG256 1
+#endif
 
-// Column tile geometry per (N, columns C); C = 8 -> 128-byte rows, SWIZZLE_128B; C = 4 ->
-// 64-byte rows, SWIZZLE_64B.  G consumer groups work on consecutive tiles independently
-// (own named barrier), so one group's barrier waits overlap another group's arithmetic.
-template <int N, int C_, int G_>
+// Column tile geometry: C columns (C = 8 -> 128-byte rows, SWIZZLE_128B; C = 4 -> 64-byte
+// rows, SWIZZLE_64B), N rows, NC components (3 when the tile is solved, 1 for the y passes),
+// S ring stages; G consumer groups work on consecutive tiles independently (own named
+// barrier), so one group's barrier waits overlap another group's arithmetic.
+template <int N, int C_, int G_, int NC_, int S_>
 struct CT {
-  static constexpr int C = C_, G = G_;
+  static constexpr int C = C_, G = G_, NC = NC_, STAGES = S_;
   static constexpr int T = Plan<N>::T;                 // threads per pencil
-  static constexpr int NTG = 3 * C * T;                // consumer threads per group
+  static constexpr int NTG = NC * C * T;               // consumer threads per group
   static constexpr int NT = G * NTG;                   // consumer threads
   static constexpr int NTHR = NT + 32;                 // + one producer warp
   static constexpr int TILE = N * C;                   // complex per component
-  static constexpr uint32_t STAGE_BYTES = 3u * TILE * 16u;
-  static constexpr int STAGES = 2 * G;
+  static constexpr uint32_t STAGE_BYTES = (uint32_t)NC * TILE * 16u;
+  static constexpr int BOXR = N < 256 ? N : 256;       // TMA box rows (<= 256)
   static constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024;
   static_assert(NTG % 32 == 0, "named barriers need whole warps");
   static_assert(SMEM <= 227 * 1024, "shared memory");
 };
-// which (C, G) each pass uses: the y passes touch the large-pitch side of S2 (ky stride
-// N*P*16 B), where 128-byte rows are needed for DRAM efficiency (tools/membench.cu); the
-// z passes stay on the small pitch, where 64-byte rows stream at full rate.
+// Per pass: the y passes touch the large-pitch side of S2 (ky stride N*P*16 B), where
+// 128-byte rows are needed for DRAM efficiency (tools/membench.cu), and transform each
+// component independently (NC = 1, more, smaller stages); the z passes need the 3
+// components of a mode together (NC = 3) and stay on the small pitch, where 64-byte rows
+// stream at full rate.
 template <int N, int MODE> struct ColCfg {
   static constexpr bool ZM = MODE == MODE_Z || MODE == MODE_ZFWD || MODE == MODE_ZINV;
   static constexpr int C = (ZM && N >= 128) ? 4 : 8;
-  static constexpr int G = (ZM && N >= 128) ? 2 : 1;
+#ifdef IBK_Y256_NC3   // dev experiment: y passes at N = 256 with 3-component tiles
+  static constexpr int NC = (ZM || N == 256) ? 3 : 1;
+  static constexpr int G = ZM ? (N == 128 || N == 256 ? 2 : 1) : (N >= 512 ? 1 : (N == 256 ? 1 : 4));
+#else
+  static constexpr int NC = ZM ? 3 : 1;
+  static constexpr int G = ZM ? (N == 128 || N == 256 ? 2 : 1) : (N >= 512 ? 1 : (N == 256 ? IBK_YG256 : 4));
+#endif
+  static constexpr size_t SB = (size_t)NC * N * C * 16;
+  static constexpr int S0 = (int)((200 * 1024) / SB);
+  static constexpr int S = S0 > 2 * G + 1 ? 2 * G + 1 : S0;
+  using K = CT<N, C, G, NC, S>;
 };
 
 // Tile element (row e, column col) in 16-byte units under the TMA swizzle of the C-wide box.
@@ -107,20 +123,21 @@ __device__ __forceinline__ void fft_inplace(ACC A, int t, const double2 *__restr
 }
 
 template <int N, int MODE>
-__global__ void __launch_bounds__(CT<N, ColCfg<N, MODE>::C, ColCfg<N, MODE>::G>::NTHR, 1)
+__global__ void __launch_bounds__(ColCfg<N, MODE>::K::NTHR, 1)
 k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
          const __grid_constant__ CUtensorMap map_st, double2 *pspec,
          const double2 *__restrict__ twN, const double *__restrict__ sym_s,
          const double *__restrict__ sym_l) {
-  using K = CT<N, ColCfg<N, MODE>::C, ColCfg<N, MODE>::G>;
+  using K = typename ColCfg<N, MODE>::K;
   constexpr int C = K::C, G = K::G, T = K::T, NTG = K::NTG, NT = K::NT, S = K::STAGES;
+  constexpr int NC = K::NC, BR = K::BOXR;
   constexpr int M = N / 2, NB = (M + 1 + C - 1) / C;
   extern __shared__ __align__(1024) double2 smraw[];
   __shared__ uint64_t full[S], done[S];
   // 1024-byte aligned ring (swizzle atoms); offset arithmetic on the __shared__ array
   // keeps every tile access an LDS/STS (a uintptr_t round trip would make them generic)
   double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
-  const int ntiles = NB * N;
+  const int ntiles = NB * N * (NC == 1 ? 3 : 1);      // NC = 1: (kx block, w, comp) tiles
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
     fence_mbar_init();
@@ -133,22 +150,27 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
     if (threadIdx.x == NT) {
       prefetch_tmap(&map_ld);
       prefetch_tmap(&map_st);
+      // tile -> (x offset in doubles, w = ky or z, first component); boxes of BR rows
       auto load = [&](int tile, int s) {
-        const int x = 2 * C * (tile % NB), w = tile / NB;
-        double2 *b = stage0 + (size_t)s * 3 * K::TILE;
+        const int x = 2 * C * (tile % NB), w = NC == 1 ? (tile / NB) % N : tile / NB, c0 = NC == 1 ? tile / (NB * N) : 0;
+        double2 *b = stage0 + (size_t)s * NC * K::TILE;
         mbar_expect_tx(&full[s], K::STAGE_BYTES);
-        for (int c = 0; c < 3; ++c) {
-          if (LD3) tma_load_3d(b + c * K::TILE, &map_ld, x, w, c * N, &full[s]);
-          else     tma_load_2d(b + c * K::TILE, &map_ld, x, (c * N + w) * N, &full[s]);
-        }
+        for (int c = 0; c < NC; ++c)
+          for (int r0 = 0; r0 < N; r0 += BR) {
+            double2 *d = b + c * K::TILE + r0 * C;
+            if (LD3) tma_load_3d(d, &map_ld, x, w, (c0 + c) * N + r0, &full[s]);
+            else     tma_load_2d(d, &map_ld, x, ((c0 + c) * N + w) * N + r0, &full[s]);
+          }
       };
       auto store = [&](int tile, int s) {
-        const int x = 2 * C * (tile % NB), w = tile / NB;
-        const double2 *b = stage0 + (size_t)s * 3 * K::TILE;
-        for (int c = 0; c < 3; ++c) {
-          if (ST3) tma_store_3d(&map_st, x, w, c * N, b + c * K::TILE);
-          else     tma_store_2d(&map_st, x, (c * N + w) * N, b + c * K::TILE);
-        }
+        const int x = 2 * C * (tile % NB), w = NC == 1 ? (tile / NB) % N : tile / NB, c0 = NC == 1 ? tile / (NB * N) : 0;
+        const double2 *b = stage0 + (size_t)s * NC * K::TILE;
+        for (int c = 0; c < NC; ++c)
+          for (int r0 = 0; r0 < N; r0 += BR) {
+            const double2 *d = b + c * K::TILE + r0 * C;
+            if (ST3) tma_store_3d(&map_st, x, w, (c0 + c) * N + r0, d);
+            else     tma_store_2d(&map_st, x, ((c0 + c) * N + w) * N + r0, d);
+          }
         bulk_commit();
       };
       int i = 0;
@@ -178,12 +200,12 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G) {
     const int s = i % S;
     mbar_wait(&full[s], (i / S) & 1);
-    double2 *buf = stage0 + (size_t)s * 3 * K::TILE;
+    double2 *buf = stage0 + (size_t)s * NC * K::TILE;
     double2 *pc = buf + comp * K::TILE;
     auto A = [pc, col](int e) -> double2 & { return pc[swz<C>(e, col)]; };
     if (MODE == MODE_Z) {
       fft_inplace<N, -1, C>(A, t, twN, bar, NTG);
-      const int kx0 = C * (tile % NB), ky = tile / NB;
+      const int kx0 = C * (tile % NB), ky = tile / NB;   // NC = 3 here
       const double sy = sym_s[ky], ly = sym_l[ky];
       const bool ny = (ky == 0) || (ky == M);
       const double invV = 1.0 / ((double)N * (double)N * (double)N);
@@ -252,15 +274,16 @@ static bool encode(CUtensorMap *m, void *base, int rank, const FluidGeom &g, int
   dims[0] = (cuuint64_t)2 * (g.M + 1);
   strides[0] = (cuuint64_t)g.P * 16;
   box[0] = (cuuint32_t)(2 * C);
+  const cuuint32_t br = (cuuint32_t)(N < 256 ? N : 256);
   if (rank == 2) {
     dims[1] = (cuuint64_t)3 * N * N;
-    box[1] = (cuuint32_t)N;
+    box[1] = br;
   } else {
     dims[1] = (cuuint64_t)N;                 // z
     dims[2] = (cuuint64_t)3 * N;             // comp*N + ky
     strides[1] = (cuuint64_t)N * g.P * 16;
     box[1] = 1;
-    box[2] = (cuuint32_t)N;
+    box[2] = br;
   }
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, base, dims, strides, box, es,
                   CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -269,9 +292,9 @@ static bool encode(CUtensorMap *m, void *base, int rank, const FluidGeom &g, int
   return r == CUDA_SUCCESS;
 }
 
-static int zcols(int N) { return N >= 128 ? 4 : 8; }
+static int zcols(int N) { return N >= 128 ? 4 : 8; }   // = ColCfg<N, MODE_Z>::C
 
-bool colfft_supported(int N) { return N >= 64 && N <= 256; }
+bool colfft_supported(int N) { return N >= 64 && N <= 512; }
 
 bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m) {
   return colfft_supported(g.N) && encode(m, base, 2, g, zcols(g.N));
@@ -301,7 +324,7 @@ template <int N, int MODE>
 static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
                                    const CUtensorMap &st, double2 *pspec, const double2 *twN,
                                    const double *s_, const double *l_, cudaStream_t s) {
-  using K = CT<N, ColCfg<N, MODE>::C, ColCfg<N, MODE>::G>;
+  using K = typename ColCfg<N, MODE>::K;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(k_colfft<N, MODE>,
@@ -310,7 +333,7 @@ static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
     attr = true;
   }
   constexpr int NB = (N / 2 + 1 + K::C - 1) / K::C;   // tiles per w
-  const int grid = one_per_sm_grid(k_colfft<N, MODE>, K::NTHR, K::SMEM, NB * N);
+  const int grid = one_per_sm_grid(k_colfft<N, MODE>, K::NTHR, K::SMEM, NB * N * (K::NC == 1 ? 3 : 1));
   k_colfft<N, MODE><<<grid, K::NTHR, K::SMEM, s>>>(g, ld, st, pspec, twN, s_, l_);
   return cudaGetLastError();
 }
@@ -319,7 +342,7 @@ template <int N>
 static cudaError_t colfft_n(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
                             const double2 *twN, const double *s_, const double *l_,
                             cudaStream_t s) {
-  if constexpr (N >= 64 && N <= 256) {
+  if constexpr (N >= 64 && N <= 512) {
     if (mode == MODE_ZINV) return launch_colfft_n<N, MODE_ZINV>(g, m.s2_2d, m.s2_2d, nullptr, twN, s_, l_, s);
     if (mode == MODE_ZFWD) return launch_colfft_n<N, MODE_ZFWD>(g, m.s2_2d, m.s2_2d, nullptr, twN, s_, l_, s);
     if (mode == MODE_Z) return launch_colfft_n<N, MODE_Z>(g, m.s2_2d, m.s2_2d, pspec, twN, s_, l_, s);
@@ -337,6 +360,7 @@ cudaError_t launch_colfft(const FluidGeom &g, int mode, const TmaMaps &m, double
     case 64: return colfft_n<64>(g, mode, m, pspec, twN, sym_s, sym_l, s);
     case 128: return colfft_n<128>(g, mode, m, pspec, twN, sym_s, sym_l, s);
     case 256: return colfft_n<256>(g, mode, m, pspec, twN, sym_s, sym_l, s);
+    case 512: return colfft_n<512>(g, mode, m, pspec, twN, sym_s, sym_l, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -175,6 +175,14 @@ def test_config4_step_parity(ibm, olib):
     print(_parity(ibm, olib, make_config(4)))
 
 
+@pytest.mark.slow
+def test_config5_step_parity(ibm, olib):
+    """BASELINE.json configs[4]: 512^3, 8.4M points, random initial flow.  The oracle needs
+    ~30 s per step here, so parity is checked after 1 and 2 steps (1e-11; the 10-step bound
+    of north_star is exercised on configs 1-4)."""
+    print(_parity(ibm, olib, make_config(5), steps=(1, 1), tol=(1e-11, 1e-11)))
+
+
 @pytest.mark.parametrize("k", [1, 2])
 def test_interpolated_velocity_parity(ibm, olib, k):
     """U at the step's positions (Z4): the high-precision check behind X."""
