@@ -24,8 +24,11 @@ STAGE_OF = [("k_force_spread", "force_spread"), ("k_drive_spread", "force_spread
             ("k_xfwd", "xfwd_rhs_r2c"), ("k_ypass<256, (int)-1>", "y_fwd"),
             ("k_ypass<(int)256, (int)-1>", "y_fwd"), ("k_ypass<256, 1>", "y_inv"),
             ("k_ypass<(int)256, (int)1>", "y_inv"), ("k_zpass", "z_solve"),
-            ("k_yz", "yz_solve"), ("k_xinv", "xinv_c2r"), ("k_interp", "interp_update"),
-            ("k_spread", "force_spread"), ("k_bin", "force_spread")]
+            ("k_colfft<256, 1>", "y_fwd"), ("k_colfft<256, 0>", "z_solve"),
+            ("k_colfft<256, 2>", "y_inv"), ("k_colfft<(int)256, (int)1>", "y_fwd"),
+            ("k_colfft<(int)256, (int)0>", "z_solve"), ("k_colfft<(int)256, (int)2>", "y_inv"),
+            ("k_xinv", "xinv_c2r"), ("k_interp", "interp_update"), ("k_step_inc", "step_inc"),
+            ("k_bin", "binning"), ("k_scan", "binning")]
 
 
 def stage(name):
