@@ -263,3 +263,20 @@ def test_empty_structure_and_smallest_grid(ibm, olib):
         u, _ = c.get_fields()
         assert np.max(np.abs(u)) == 0.0
         assert c.get_positions().shape == (0, 3)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3, 4, 5])
+def test_config_full_length_stays_finite_and_bounded(ibm, k):
+    """Each BASELINE.json config for its stated step count (10/100/400/200/50) on the GPU:
+    ib_step reports no non-finite state, and velocity / displacement stay bounded."""
+    cfg = make_config(k)
+    with ibm.IBContext.from_config(cfg) as c:
+        c.step(cfg.steps)
+        assert c.n == cfg.steps
+        u, _ = c.get_fields()
+        X = c.get_positions()
+    assert np.isfinite(u).all() and np.isfinite(X).all()
+    umax = float(np.max(np.abs(u)))
+    dmax = float(np.max(np.abs(X - cfg.X)))
+    print(f"cfg{k}: {cfg.steps} steps, max|u| {umax:.3e}, max|X-X0| {dmax:.3e}")
+    assert umax < 100.0 and dmax < 0.5 * cfg.N * cfg.h
