@@ -273,65 +273,123 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
 }
 
 // ------------------------------------------------------------------ interp + update
-__global__ void __launch_bounds__(256)
-k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
-         long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm) {
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  bool bad = false;
-  if (k < np) {
-    // cell-binned order: the lanes of a warp mostly share one 4x4x4 support box, so the
-    // 192 gathers of a warp hit the same L1 lines (broadcast)
-    const int64_t i = perm ? (int64_t)__ldg(&perm[k]) : k;
-    const int N = g.N;
-    const size_t V = (size_t)g.V;
-    const double x0 = X[3 * i + 0], x1 = X[3 * i + 1], x2 = X[3 * i + 2];
-    double wx[4], wy[4], wz[4];
-    const int jx = axis_weights(x0, g.invh, wx);
-    const int jy = axis_weights(x1, g.invh, wy);
-    const int jz = axis_weights(x2, g.invh, wz);
-    // U = sum_c wz_c sum_b wy_b (sum_a wx_a u(jx+a, jy+b, jz+c)): row sums first (4 FMAs
-    // per row and component), 32-bit cell offsets (3V < 2^31 for N <= 512); a row with no
-    // periodic wrap in x (the common case) is 4 consecutive doubles off one base pointer
-    int ro[4][4];
+// U = sum_c wz_c sum_b wy_b (sum_a wx_a u(jx+a, jy+b, jz+c)) straight from global memory
+// (row sums first, 32-bit cell offsets; a row with no periodic wrap in x is 4 consecutive
+// doubles off one base pointer).  Used by warps whose points span more than BOXES boxes.
+__device__ __forceinline__ void interp_direct(const double *__restrict__ u, int N, int Vi,
+                                              int jx, int jy, int jz, const double wx[4],
+                                              const double wy[4], const double wz[4],
+                                              double &U0, double &U1, double &U2) {
+  int ro[4][4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      ro[c][b] = (((jz + c) & (N - 1)) * N + ((jy + b) & (N - 1))) * N;
+  U0 = U1 = U2 = 0.0;
+  if (jx >= 0 && jx + 3 < N) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
-      for (int b = 0; b < 4; ++b)
-        ro[c][b] = (((jz + c) & (N - 1)) * N + ((jy + b) & (N - 1))) * N;
-    double U0 = 0.0, U1 = 0.0, U2 = 0.0;
-    const int Vi = (int)V;
-    if (jx >= 0 && jx + 3 < N) {
+      for (int b = 0; b < 4; ++b) {
+        const double *r0 = u + (ro[c][b] + jx), *r1 = r0 + Vi, *r2 = r1 + Vi;
+        const double s0 = wx[0] * __ldg(r0) + wx[1] * __ldg(r0 + 1) + wx[2] * __ldg(r0 + 2) + wx[3] * __ldg(r0 + 3);
+        const double s1 = wx[0] * __ldg(r1) + wx[1] * __ldg(r1 + 1) + wx[2] * __ldg(r1 + 2) + wx[3] * __ldg(r1 + 3);
+        const double s2 = wx[0] * __ldg(r2) + wx[1] * __ldg(r2 + 1) + wx[2] * __ldg(r2 + 2) + wx[3] * __ldg(r2 + 3);
+        const double wbc = wy[b] * wz[c];
+        U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
+      }
+  } else {
+    int xo[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
+    for (int a = 0; a < 4; ++a) xo[a] = (jx + a) & (N - 1);
 #pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const double *r0 = u + (ro[c][b] + jx), *r1 = r0 + Vi, *r2 = r1 + Vi;
-          const double s0 = wx[0] * __ldg(r0) + wx[1] * __ldg(r0 + 1) + wx[2] * __ldg(r0 + 2) + wx[3] * __ldg(r0 + 3);
-          const double s1 = wx[0] * __ldg(r1) + wx[1] * __ldg(r1 + 1) + wx[2] * __ldg(r1 + 2) + wx[3] * __ldg(r1 + 3);
-          const double s2 = wx[0] * __ldg(r2) + wx[1] * __ldg(r2 + 1) + wx[2] * __ldg(r2 + 2) + wx[3] * __ldg(r2 + 3);
-          const double wbc = wy[b] * wz[c];
-          U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) {
+        const double *r0 = u + ro[c][b], *r1 = r0 + Vi, *r2 = r1 + Vi;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          s0 += wx[a] * __ldg(r0 + xo[a]);
+          s1 += wx[a] * __ldg(r1 + xo[a]);
+          s2 += wx[a] * __ldg(r2 + xo[a]);
         }
-    } else {
-      int xo[4];
+        const double wbc = wy[b] * wz[c];
+        U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
+      }
+  }
+}
+
+// One thread per point in cell-binned order.  A warp whose 32 points use at most BOXES
+// distinct 4x4x4 support boxes (the common case after binning) loads each box once,
+// cooperatively (lane = (a, b, c0): nodes (a, b, c0) and (a, b, c0 + 2), 3 components),
+// into shared memory; each lane then sums its point from its box with broadcast reads.
+// Other warps gather straight from global memory.  Update X^{n+1} = X^n + dt U fused;
+// non-finite flag.
+constexpr int INTERP_THREADS = 128, BOXES = 4, BOXLD = 3 * 64 + 2;   // +2: bank shift per box
+
+__global__ void __launch_bounds__(INTERP_THREADS)
+k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
+         long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm) {
+  __shared__ double box[INTERP_THREADS / 32][BOXES][BOXLD];
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int N = g.N;
+  const int Vi = (int)g.V;
+  const bool live = k < np;
+  bool bad = false;
+  const int64_t i = live ? (perm ? (int64_t)__ldg(&perm[k]) : k) : 0;
+  double x0 = 0.5 * g.h, x1 = 0.5 * g.h, x2 = 0.5 * g.h;
+  if (live) { x0 = X[3 * i + 0]; x1 = X[3 * i + 1]; x2 = X[3 * i + 2]; }
+  double wx[4], wy[4], wz[4];
+  const int jx = axis_weights(x0, g.invh, wx);
+  const int jy = axis_weights(x1, g.invh, wy);
+  const int jz = axis_weights(x2, g.invh, wz);
+  const unsigned key = ((unsigned)(jz & (N - 1)) * N + (unsigned)(jy & (N - 1))) * N + (unsigned)(jx & (N - 1));
+  const unsigned active = __ballot_sync(0xffffffffu, live);
+  const unsigned peers = __match_any_sync(0xffffffffu, live ? key : 0xffffffffu) & active;
+  const unsigned leaders = __ballot_sync(0xffffffffu, live && lane == __ffs(peers) - 1);
+  double U0, U1, U2;
+  if (__popc(leaders) <= BOXES) {
+    const int a = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
+    unsigned lm = leaders;
+    for (int gi = 0; lm; ++gi) {
+      const int ld = __ffs(lm) - 1;
+      lm &= lm - 1;
+      const int gx = __shfl_sync(0xffffffffu, jx, ld), gy = __shfl_sync(0xffffffffu, jy, ld),
+                gz = __shfl_sync(0xffffffffu, jz, ld);
+      const int xo = (gx + a) & (N - 1), yo = (gy + b) & (N - 1);
+      double *bx = box[warp][gi];
 #pragma unroll
-      for (int a = 0; a < 4; ++a) xo[a] = (jx + a) & (N - 1);
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-          const double *r0 = u + ro[c][b], *r1 = r0 + Vi, *r2 = r1 + Vi;
-          double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            s0 += wx[a] * __ldg(r0 + xo[a]);
-            s1 += wx[a] * __ldg(r1 + xo[a]);
-            s2 += wx[a] * __ldg(r2 + xo[a]);
-          }
-          const double wbc = wy[b] * wz[c];
-          U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
-        }
+      for (int h = 0; h < 2; ++h) {
+        const int c = c0 + 2 * h;
+        const int cell = (((gz + c) & (N - 1)) * N + yo) * N + xo;
+        const int node = (c * 4 + b) * 4 + a;
+        bx[node] = __ldg(u + cell);
+        bx[64 + node] = __ldg(u + Vi + cell);
+        bx[128 + node] = __ldg(u + 2 * Vi + cell);
+      }
     }
+    __syncwarp();
+    const int mine = __popc(leaders & ((1u << (__ffs(peers) - 1)) - 1u));
+    const double *bx = box[warp][live ? mine : 0];
+    U0 = U1 = U2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        const double *r = bx + (c * 4 + bb) * 4;
+        const double s0 = wx[0] * r[0] + wx[1] * r[1] + wx[2] * r[2] + wx[3] * r[3];
+        const double s1 = wx[0] * r[64] + wx[1] * r[65] + wx[2] * r[66] + wx[3] * r[67];
+        const double s2 = wx[0] * r[128] + wx[1] * r[129] + wx[2] * r[130] + wx[3] * r[131];
+        const double wbc = wy[bb] * wz[c];
+        U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
+      }
+  } else {
+    interp_direct(u, N, Vi, jx, jy, jz, wx, wy, wz, U0, U1, U2);
+  }
+  if (live) {
     if (U_out) {
       U_out[3 * i + 0] = U0; U_out[3 * i + 1] = U1; U_out[3 * i + 2] = U2;
     } else {
@@ -350,8 +408,8 @@ cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_
                           double *U_out, long long *flag, const long long *dev_n, long long n,
                           const int *perm, cudaStream_t s) {
   if (np > 0)
-    k_interp<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(g, u, X, np, U_out, flag, dev_n, n,
-                                                          perm);
+    k_interp<<<(unsigned)((np + INTERP_THREADS - 1) / INTERP_THREADS), INTERP_THREADS, 0, s>>>(
+        g, u, X, np, U_out, flag, dev_n, n, perm);
   return cudaGetLastError();
 }
 
