@@ -16,6 +16,7 @@
 
 #include "fft.cuh"
 #include "ib_internal.cuh"
+#include "tma.cuh"
 
 namespace ibk {
 
@@ -89,10 +90,15 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(3 * XCfg<N>::RB * XCfg<N>::T)
 k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
        const double *__restrict__ in, double *r_out, double2 *spec,
-       const double2 *__restrict__ twN, const double2 *__restrict__ twM) {
+       const double2 *__restrict__ twN, const double2 *__restrict__ twM,
+       const __grid_constant__ CUtensorMap map_rows, const __grid_constant__ CUtensorMap map_row1,
+       int use_tma) {
   constexpr int M = N / 2, RB = XCfg<N>::RB, T = XCfg<N>::T, LD = Plan<M>::LD;
   constexpr int NC = MODE == 2 ? 1 : 3, UR = RB + 2;
-  extern __shared__ double2 sm[];
+  extern __shared__ __align__(128) double2 smraw_x[];
+  __shared__ uint64_t tbar;
+  // 128-byte aligned tile (TMA destination); offset arithmetic keeps accesses LDS/STS
+  double2 *sm = smraw_x + ((128u - (smem_u32(smraw_x) & 127u)) & 127u) / 16u;
   double *ut = reinterpret_cast<double *>(sm);     // u tile [comp][UR][N]
   const int z = blockIdx.y, y0 = blockIdx.x * RB;
   const int t = threadIdx.x % T, pencil = threadIdx.x / T;
@@ -100,7 +106,21 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   const size_t V = (size_t)N * N * N;
   const size_t rowbase = ((size_t)z * N + y) * N;
   const double cu = g.rho / g.dt, ra = g.rho * g.invh;
-  if (MODE != 2) {
+  if (MODE != 2 && use_tma) {   // one thread streams the 3 x (RB + 2) rows with TMA
+    if (threadIdx.x == 0) {
+      mbar_init(&tbar, 1);
+      fence_mbar_init();
+      mbar_expect_tx(&tbar, (uint32_t)(3 * UR * N * 8));
+      for (int c = 0; c < 3; ++c) {
+        const int rb = (c * N + z) * N;
+        tma_load_2d(ut + ((size_t)c * UR + 1) * N, &map_rows, 0, rb + y0, &tbar);
+        tma_load_2d(ut + (size_t)c * UR * N, &map_row1, 0, rb + ((y0 - 1 + N) & (N - 1)), &tbar);
+        tma_load_2d(ut + ((size_t)c * UR + RB + 1) * N, &map_row1, 0, rb + ((y0 + RB) & (N - 1)), &tbar);
+      }
+    }
+    __syncthreads();                                // barrier initialised before anyone waits
+    mbar_wait(&tbar, 0);
+  } else if (MODE != 2) {
     constexpr int CH = N / 2;                      // 16-byte chunks per row
     for (int idx = threadIdx.x; idx < 3 * UR * CH; idx += blockDim.x) {
       const int ch = idx % CH, rr = (idx / CH) % UR, cc = idx / (CH * UR);
@@ -188,20 +208,24 @@ template <int N>
 static cudaError_t launch_xfwd_n(const FluidGeom &g, int mode, const double *u, double *F,
                                  unsigned *rowflag, const double *in, double *r_out,
                                  double2 *spec, const double2 *twN, const double2 *twM,
-                                 cudaStream_t s) {
+                                 const XMapsU *um, cudaStream_t s) {
   using X = XCfg<N>;
   dim3 grid(N / X::RB, N);
   const int nc = mode == 2 ? 1 : 3;
   const size_t fft = (size_t)nc * X::RB * Plan<N / 2>::LD * sizeof(double2);
   const size_t tile = mode == 2 ? 0 : (size_t)3 * (X::RB + 2) * N * sizeof(double);
-  const size_t smem = fft > tile ? fft : tile;
+  const size_t smem = (fft > tile ? fft : tile) + 128;
   const int threads = nc * X::RB * X::T;
+  // TMA row boxes (N <= 256 doubles per box) when the caller encoded maps of u
+  CUtensorMap rows{}, row1{};
+  const int use_tma = (mode != 2 && um && um->ok) ? 1 : 0;
+  if (use_tma) { rows = um->rows; row1 = um->row1; }
   if (mode == 0)
-    k_xfwd<N, 0><<<grid, threads, smem, s>>>(g, u, F, rowflag, in, r_out, spec, twN, twM);
+    k_xfwd<N, 0><<<grid, threads, smem, s>>>(g, u, F, rowflag, in, r_out, spec, twN, twM, rows, row1, use_tma);
   else if (mode == 1)
-    k_xfwd<N, 1><<<grid, threads, smem, s>>>(g, u, F, nullptr, in, r_out, spec, twN, twM);
+    k_xfwd<N, 1><<<grid, threads, smem, s>>>(g, u, F, nullptr, in, r_out, spec, twN, twM, rows, row1, use_tma);
   else
-    k_xfwd<N, 2><<<grid, threads, smem, s>>>(g, u, F, nullptr, in, r_out, spec, twN, twM);
+    k_xfwd<N, 2><<<grid, threads, smem, s>>>(g, u, F, nullptr, in, r_out, spec, twN, twM, rows, row1, 0);
   return cudaGetLastError();
 }
 
@@ -471,8 +495,9 @@ static cudaError_t launch_xinv_n(const FluidGeom &g, const double2 *spec, double
 
 cudaError_t launch_xfwd(const FluidGeom &g, int mode, const double *u, double *F,
                         unsigned *rowflag, const double *in, double *r_out, double2 *spec,
-                        const double2 *twN, const double2 *twM, cudaStream_t s) {
-#define CALL(n) launch_xfwd_n<n>(g, mode, u, F, rowflag, in, r_out, spec, twN, twM, s)
+                        const double2 *twN, const double2 *twM, const XMapsU *um,
+                        cudaStream_t s) {
+#define CALL(n) launch_xfwd_n<n>(g, mode, u, F, rowflag, in, r_out, spec, twN, twM, um, s)
   IBK_DISPATCH_N(g.N, CALL)
 #undef CALL
 }
@@ -499,6 +524,39 @@ cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, in
 #define CALL(n_) launch_xinv_n<n_>(g, spec, out, ncomp, twN, twM, flag, dev_n, n, s)
   IBK_DISPATCH_N(g.N, CALL)
 #undef CALL
+}
+
+// TMA descriptors of a u-shaped array [3][N][N][N]: RB-row and 1-row boxes of full x rows.
+bool xfwd_encode_u(const FluidGeom &g, const double *u, XMapsU *m) {
+  m->ok = false;
+  const int N = g.N;
+  if (N > 256 || N < 16) return false;     // box <= 256 doubles; rows >= 128 B (smem alignment)
+  void *p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
+                                       &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return false;
+  auto fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  int rb = 0;
+  switch (N) {
+    case 8: rb = XCfg<8>::RB; break;      case 16: rb = XCfg<16>::RB; break;
+    case 32: rb = XCfg<32>::RB; break;    case 64: rb = XCfg<64>::RB; break;
+    case 128: rb = XCfg<128>::RB; break;  case 256: rb = XCfg<256>::RB; break;
+    default: return false;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)3 * N * N}, strides[1] = {(cuuint64_t)N * 8};
+  cuuint32_t box[2] = {(cuuint32_t)N, (cuuint32_t)rb}, box1[2] = {(cuuint32_t)N, 1u}, es[2] = {1, 1};
+  void *base = const_cast<double *>(u);
+  if (fn(&m->rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  if (fn(&m->row1, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box1, es,
+         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  m->ok = true;
+  return true;
 }
 
 template <int N>

@@ -137,8 +137,15 @@ size_t pspec_elems(const ib_ctx *c) {
 cudaError_t xfwd(ib_ctx *c, int mode, const double *u, double *F, unsigned *rowflag,
                  double *r_out, cudaStream_t s) {
   if (mode == 2)
-    return launch_xfwd(c->g, 2, nullptr, nullptr, nullptr, u, nullptr, c->spec, c->twN, c->twM, s);
-  return launch_xfwd(c->g, mode, u, F, rowflag, nullptr, r_out, c->spec, c->twN, c->twM, s);
+    return launch_xfwd(c->g, 2, nullptr, nullptr, nullptr, u, nullptr, c->spec, c->twN, c->twM,
+                       nullptr, s);
+  XMapsU tmp;
+  const XMapsU *um = &c->umaps;
+  if (u != c->u) {                      // debug arrays: maps encoded on the fly
+    xfwd_encode_u(c->g, u, &tmp);
+    um = &tmp;
+  }
+  return launch_xfwd(c->g, mode, u, F, rowflag, nullptr, r_out, c->spec, c->twN, c->twM, um, s);
 }
 cudaError_t xinv(ib_ctx *c, double *out, const long long *dev_n, long long n, long long *flag,
                  cudaStream_t s) {
@@ -262,6 +269,9 @@ ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
   if ((e = cudaMemsetAsync(c->F, 0, 3 * V * sizeof(double), c->stream)) != cudaSuccess) return bad(e, "memset");
   if ((e = fluid_setup_attributes(N)) != cudaSuccess) return bad(e, "attributes");
   if ((e = colfft_make_maps(c->g, c->spec, c->spec2, &c->maps)) != cudaSuccess) return bad(e, "TMA tensor maps");
+#ifndef IBK_NO_XFTMA
+  xfwd_encode_u(c->g, c->u, &c->umaps);   // !ok (cp.async tile copy) when N > 256
+#endif
 #ifndef IBK_NO_XTMA   // dev switch: the per-CTA row kernels of fluid.cu for comparison
   if (xpass_supported(N)) {
     if (!xpass_encode_s1(c->g, c->spec, &c->smaps))

@@ -39,6 +39,11 @@ struct TmaMaps {
   bool ok = false;
 };
 
+// TMA descriptors of the forward x pass (fluid.cu): u rows, RB-row and 1-row boxes.
+struct XMapsU {
+  CUtensorMap rows, row1;
+  bool ok = false;
+};
 // TMA descriptors of the inverse x pass (xpass_tma.cu): S1 spectrum rows (kx < N/2 box and
 // the Nyquist column).
 struct XMapsS {
@@ -67,6 +72,7 @@ struct ib_ctx {
   double *sym_s = nullptr, *sym_l = nullptr; // per-axis symbols
   ibk::TmaMaps maps;                         // TMA column-pass descriptors (N in [64, 256])
   ibk::XMapsS smaps;                         // TMA x-inverse descriptors of spec
+  ibk::XMapsU umaps;                         // TMA x-forward descriptors of u (N <= 256)
   bool xok = false;
   // Lagrangian state
   int64_t np = 0;
@@ -105,9 +111,12 @@ cudaError_t init_tables(ib_ctx *c);
 cudaError_t fluid_setup_attributes(int N);
 // x pass: mode 0 = step (r from u,F; zero F), 1 = r only (write r_out), 2 = FFT of in (1 comp)
 // rowflag (may be null = read all of F): per (z,y) row, set by the spread where F != 0
+// um: TMA maps of `u` (tile rows streamed by TMA) or null / !ok (cp.async tile copy)
 cudaError_t launch_xfwd(const FluidGeom &g, int mode, const double *u, double *F,
                         unsigned *rowflag, const double *in, double *r_out, double2 *spec,
-                        const double2 *twN, const double2 *twM, cudaStream_t s);
+                        const double2 *twN, const double2 *twM, const XMapsU *um,
+                        cudaStream_t s);
+bool xfwd_encode_u(const FluidGeom &g, const double *u, XMapsU *m);
 // y pass between spectrum layouts (1 = S1 [comp][z][y][kx], 2 = S2 [comp][ky][z][kx])
 cudaError_t launch_ypass(const FluidGeom &g, int sign, const double2 *in, int in_layout,
                          double2 *out, int out_layout, int ncomp, const double2 *twN,
