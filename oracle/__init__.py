@@ -45,17 +45,18 @@ def lib():
             L.ibo_phi.argtypes = [d]
             L.ibo_set_threads.argtypes = [C.c_int]
             L.ibo_get_threads.restype = C.c_int
+            n3 = [i32, i32, i32]
             L.ibo_force.argtypes = [p, i64, i32, p, p, p, p, p, p, i64, p, p, d, i32, i64, p]
-            L.ibo_spread.argtypes = [i32, d, p, p, i64, p]
-            L.ibo_interp.argtypes = [i32, d, p, p, i64, p]
-            L.ibo_advect.argtypes = [i32, d, p, p]
-            L.ibo_rhs.argtypes = [i32, d, d, d, p, p, p]
-            L.ibo_fft3.argtypes = [i32, p, p, C.c_int]
-            L.ibo_solve.argtypes = [i32, d, d, d, d, p, p, p]
-            L.ibo_fluid_step.argtypes = [i32, d, d, d, d, p, p, p, p]
+            L.ibo_spread.argtypes = n3 + [d, p, p, i64, p]
+            L.ibo_interp.argtypes = n3 + [d, p, p, i64, p]
+            L.ibo_advect.argtypes = n3 + [d, p, p]
+            L.ibo_rhs.argtypes = n3 + [d, d, d, p, p, p]
+            L.ibo_fft3.argtypes = n3 + [p, p, C.c_int]
+            L.ibo_solve.argtypes = n3 + [d, d, d, d, p, p, p]
+            L.ibo_fluid_step.argtypes = n3 + [d, d, d, d, p, p, p, p]
             L.ibo_step.restype = C.c_int
-            L.ibo_step.argtypes = [i32, d, d, d, d, p, p, p, i64, i32, p, p, p, p, p, p,
-                                   i64, p, p, d, i32, i64, i32]
+            L.ibo_step.argtypes = n3 + [d, d, d, d, p, p, p, i64, i32, p, p, p, p, p, p,
+                                        i64, p, p, d, i32, i64, i32, i32]
             _lib = L
     return _lib
 
@@ -69,6 +70,20 @@ def _f64(a, shape=None):
     if shape is not None:
         a = a.reshape(shape)
     return a
+
+
+def dims(N):
+    """(N1, N2, N3) = lattice points along x, y, z from an int (cubic) or a 3-sequence."""
+    if isinstance(N, (tuple, list, np.ndarray)):
+        n1, n2, n3 = (int(v) for v in N)
+        return n1, n2, n3
+    return int(N), int(N), int(N)
+
+
+def fshape(N):
+    """Field array shape [3][N3][N2][N1]."""
+    n1, n2, n3 = dims(N)
+    return (3, n3, n2, n1)
 
 
 def set_threads(n: int) -> None:
@@ -117,65 +132,69 @@ def force(X, patches, stiffness, step=0, drive_idx=None, drive_dir=None, drive_a
 
 def spread(N, h, X, Fnode) -> np.ndarray:
     X = _f64(X, (-1, 3)); Fn = _f64(Fnode, (-1, 3))
-    F = np.empty((3, N, N, N))
-    lib().ibo_spread(N, h, _ptr(X), _ptr(Fn), X.shape[0], _ptr(F))
+    F = np.empty(fshape(N))
+    lib().ibo_spread(*dims(N), h, _ptr(X), _ptr(Fn), X.shape[0], _ptr(F))
     return F
 
 
 def interp(N, h, u, X) -> np.ndarray:
-    X = _f64(X, (-1, 3)); u = _f64(u, (3, N, N, N))
+    X = _f64(X, (-1, 3)); u = _f64(u, fshape(N))
     U = np.empty_like(X)
-    lib().ibo_interp(N, h, _ptr(u), _ptr(X), X.shape[0], _ptr(U))
+    lib().ibo_interp(*dims(N), h, _ptr(u), _ptr(X), X.shape[0], _ptr(U))
     return U
 
 
 def advect(N, h, u) -> np.ndarray:
-    u = _f64(u, (3, N, N, N))
+    u = _f64(u, fshape(N))
     a = np.empty_like(u)
-    lib().ibo_advect(N, h, _ptr(u), _ptr(a))
+    lib().ibo_advect(*dims(N), h, _ptr(u), _ptr(a))
     return a
 
 
 def rhs(N, h, rho, dt, u, F) -> np.ndarray:
-    u = _f64(u, (3, N, N, N)); F = _f64(F, (3, N, N, N))
+    u = _f64(u, fshape(N)); F = _f64(F, fshape(N))
     r = np.empty_like(u)
-    lib().ibo_rhs(N, h, rho, dt, _ptr(u), _ptr(F), _ptr(r))
+    lib().ibo_rhs(*dims(N), h, rho, dt, _ptr(u), _ptr(F), _ptr(r))
     return r
 
 
 def fft3(x: np.ndarray, sign: int = -1) -> np.ndarray:
-    """Unnormalised 3-D DFT of a complex [N][N][N] array with the oracle's radix-2 FFT."""
+    """Unnormalised 3-D DFT of a complex [N3][N2][N1] array with the oracle's radix-2 FFT."""
     x = np.asarray(x, dtype=np.complex128)
-    N = x.shape[0]
+    n3, n2, n1 = x.shape
     re = np.ascontiguousarray(x.real); im = np.ascontiguousarray(x.imag)
-    lib().ibo_fft3(N, _ptr(re), _ptr(im), int(sign))
+    lib().ibo_fft3(n1, n2, n3, _ptr(re), _ptr(im), int(sign))
     return re + 1j * im
 
 
 def solve(N, h, rho, mu, dt, r, want_p=True):
-    r = _f64(r, (3, N, N, N))
+    r = _f64(r, fshape(N))
     u = np.empty_like(r)
-    p = np.empty((N, N, N)) if want_p else None
-    lib().ibo_solve(N, h, rho, mu, dt, _ptr(r), _ptr(u), _ptr(p))
+    p = np.empty(fshape(N)[1:]) if want_p else None
+    lib().ibo_solve(*dims(N), h, rho, mu, dt, _ptr(r), _ptr(u), _ptr(p))
     return u, p
 
 
 def fluid_step(N, h, rho, mu, dt, u, F, want_p=True):
-    u = _f64(u, (3, N, N, N)); F = _f64(F, (3, N, N, N))
+    u = _f64(u, fshape(N)); F = _f64(F, fshape(N))
     un = np.empty_like(u)
-    p = np.empty((N, N, N)) if want_p else None
-    lib().ibo_fluid_step(N, h, rho, mu, dt, _ptr(u), _ptr(F), _ptr(un), _ptr(p))
+    p = np.empty(fshape(N)[1:]) if want_p else None
+    lib().ibo_fluid_step(*dims(N), h, rho, mu, dt, _ptr(u), _ptr(F), _ptr(un), _ptr(p))
     return un, p
 
 
 class Oracle:
     """Stateful oracle with the same call sequence as the product binding
-    (create / set_structure / set_velocity / set_drive / step / get_*)."""
+    (create / set_structure / set_velocity / set_drive / step / get_*).  N is an int (cubic
+    lattice) or (N1, N2, N3)."""
 
     def __init__(self, N, h, rho, mu, dt):
-        self.N, self.h, self.rho, self.mu, self.dt = int(N), float(h), float(rho), float(mu), float(dt)
-        self.u = np.zeros((3, N, N, N))
-        self.p = np.zeros((N, N, N))
+        self.dims = dims(N)
+        self.N = N if not isinstance(N, (tuple, list)) else tuple(int(v) for v in N)
+        self.h, self.rho, self.mu, self.dt = float(h), float(rho), float(mu), float(dt)
+        self.u = np.zeros(fshape(N))
+        self.p = np.zeros(fshape(N)[1:])
+        self.p_steps = None              # [nsteps][N3][N2][N1] when step(..., p_every=True)
         self.X = np.zeros((0, 3))
         self.S = _Structure([], np.zeros(0))
         self.nd = 0
@@ -201,7 +220,7 @@ class Oracle:
         self.X = _f64(X, (-1, 3)).copy()
 
     def set_velocity(self, u):
-        self.u = _f64(u, (3, self.N, self.N, self.N)).copy()
+        self.u = _f64(u, fshape(self.dims)).copy()
 
     def set_drive(self, idx, direction, amp, period):
         self.nd = len(idx)
@@ -209,11 +228,17 @@ class Oracle:
         self.dd = _f64(direction, (-1, 3))
         self.amp, self.period = float(amp), int(period)
 
-    def step(self, nsteps=1):
-        st = lib().ibo_step(self.N, self.h, self.rho, self.mu, self.dt, _ptr(self.u),
-                            _ptr(self.p), _ptr(self.X), self.X.shape[0], *self.S.args(),
+    def step(self, nsteps=1, p_every=False):
+        """nsteps IB steps; p_every: keep p^{n+1} of every step in self.p_steps."""
+        pbuf = np.empty((int(nsteps),) + fshape(self.dims)[1:]) if p_every else self.p
+        st = lib().ibo_step(*self.dims, self.h, self.rho, self.mu, self.dt, _ptr(self.u),
+                            _ptr(pbuf), _ptr(self.X), self.X.shape[0], *self.S.args(),
                             self.nd, _ptr(self.di), _ptr(self.dd), self.amp, self.period,
-                            self.n, int(nsteps))
+                            self.n, int(nsteps), 1 if p_every else 0)
+        if p_every:
+            self.p_steps = pbuf
+            if nsteps:
+                self.p = pbuf[-1].copy()
         if st:
             self.n += st - 1
             raise FloatingPointError(f"oracle: non-finite state at step {self.n}")

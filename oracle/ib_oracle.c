@@ -133,9 +133,9 @@ static void weights(double Xa, double h, int64_t *j0, double w[4]) {
   for (int a = 0; a < 4; ++a) w[a] = ibo_phi((h * (double)(j + a) - Xa) / h);
 }
 
-void ibo_spread(int32_t N, double h, const double *X, const double *Fnode, int64_t np,
-                double *F) {
-  const size_t V = (size_t)N * N * N;
+void ibo_spread(int32_t N1, int32_t N2, int32_t N3, double h, const double *X,
+                const double *Fnode, int64_t np, double *F) {
+  const size_t V = (size_t)N1 * N2 * N3;
   const double h3 = h * h * h;
   memset(F, 0, sizeof(double) * 3 * V);
   for (int64_t q = 0; q < np; ++q) {
@@ -148,16 +148,17 @@ void ibo_spread(int32_t N, double h, const double *X, const double *Fnode, int64
       for (int b = 0; b < 4; ++b)
         for (int a = 0; a < 4; ++a) {
           double delta = wx[a] * wy[b] * wz[c] / h3;     /* delta_h(x - X(q)) */
-          size_t cell = ((size_t)wrapi(jz + c, N) * N + (size_t)wrapi(jy + b, N)) * N +
-                        (size_t)wrapi(jx + a, N);
+          size_t cell = ((size_t)wrapi(jz + c, N3) * N2 + (size_t)wrapi(jy + b, N2)) * N1 +
+                        (size_t)wrapi(jx + a, N1);
           for (int d = 0; d < 3; ++d) F[d * V + cell] += Fnode[3 * q + d] * delta;
         }
   }
 }
 
 /* ------------------------------------------------------------------ step 4: interpolate */
-void ibo_interp(int32_t N, double h, const double *u, const double *X, int64_t np, double *U) {
-  const size_t V = (size_t)N * N * N;
+void ibo_interp(int32_t N1, int32_t N2, int32_t N3, double h, const double *u, const double *X,
+                int64_t np, double *U) {
+  const size_t V = (size_t)N1 * N2 * N3;
   for (int64_t q = 0; q < np; ++q) {
     int64_t jx, jy, jz;
     double wx[4], wy[4], wz[4];
@@ -169,8 +170,8 @@ void ibo_interp(int32_t N, double h, const double *u, const double *X, int64_t n
       for (int b = 0; b < 4; ++b)
         for (int a = 0; a < 4; ++a) {
           double w = wx[a] * wy[b] * wz[c];               /* delta_h h^3 */
-          size_t cell = ((size_t)wrapi(jz + c, N) * N + (size_t)wrapi(jy + b, N)) * N +
-                        (size_t)wrapi(jx + a, N);
+          size_t cell = ((size_t)wrapi(jz + c, N3) * N2 + (size_t)wrapi(jy + b, N2)) * N1 +
+                        (size_t)wrapi(jx + a, N1);
           for (int d = 0; d < 3; ++d) acc[d] += u[d * V + cell] * w;
         }
     U[3 * q + 0] = acc[0];
@@ -180,20 +181,20 @@ void ibo_interp(int32_t N, double h, const double *u, const double *X, int64_t n
 }
 
 /* ------------------------------------------------------------------ step 3: fluid */
-void ibo_advect(int32_t N, double h, const double *u, double *adv) {
-  const int64_t V = (int64_t)N * N * N;
+void ibo_advect(int32_t N1, int32_t N2, int32_t N3, double h, const double *u, double *adv) {
+  const int64_t V = (int64_t)N1 * N2 * N3;
 #pragma omp parallel for schedule(static)
-  for (int64_t z = 0; z < N; ++z)
-    for (int64_t y = 0; y < N; ++y)
-      for (int64_t x = 0; x < N; ++x) {
-        const int64_t c0 = (z * N + y) * N + x;
+  for (int64_t z = 0; z < N3; ++z)
+    for (int64_t y = 0; y < N2; ++y)
+      for (int64_t x = 0; x < N1; ++x) {
+        const int64_t c0 = (z * N2 + y) * N1 + x;
         /* neighbours x +- h e_k, periodic */
-        const int64_t nb_m[3] = {(z * N + y) * N + (x + N - 1) % N,
-                                 (z * N + (y + N - 1) % N) * N + x,
-                                 (((z + N - 1) % N) * N + y) * N + x};
-        const int64_t nb_p[3] = {(z * N + y) * N + (x + 1) % N,
-                                 (z * N + (y + 1) % N) * N + x,
-                                 (((z + 1) % N) * N + y) * N + x};
+        const int64_t nb_m[3] = {(z * N2 + y) * N1 + (x + N1 - 1) % N1,
+                                 (z * N2 + (y + N2 - 1) % N2) * N1 + x,
+                                 (((z + N3 - 1) % N3) * N2 + y) * N1 + x};
+        const int64_t nb_p[3] = {(z * N2 + y) * N1 + (x + 1) % N1,
+                                 (z * N2 + (y + 1) % N2) * N1 + x,
+                                 (((z + 1) % N3) * N2 + y) * N1 + x};
         for (int i = 0; i < 3; ++i) {
           const double *ui = u + i * V;
           double s = 0.0;
@@ -210,11 +211,11 @@ void ibo_advect(int32_t N, double h, const double *u, double *adv) {
       }
 }
 
-void ibo_rhs(int32_t N, double h, double rho, double dt, const double *u, const double *F,
-             double *r) {
-  const int64_t V = (int64_t)N * N * N;
+void ibo_rhs(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double dt,
+             const double *u, const double *F, double *r) {
+  const int64_t V = (int64_t)N1 * N2 * N3;
   double *adv = (double *)malloc(sizeof(double) * 3 * (size_t)V);
-  ibo_advect(N, h, u, adv);
+  ibo_advect(N1, N2, N3, h, u, adv);
 #pragma omp parallel for schedule(static)
   for (int64_t c = 0; c < 3 * V; ++c) r[c] = rho * u[c] / dt - rho * adv[c] + F[c];
   free(adv);
@@ -246,24 +247,28 @@ static void fft1(int32_t N, double *re, double *im, const double *twr, const dou
   }
 }
 
-void ibo_fft3(int32_t N, double *re, double *im, int sign) {
-  double *twr = (double *)malloc(sizeof(double) * (size_t)(N / 2 + 1));
-  double *twi = (double *)malloc(sizeof(double) * (size_t)(N / 2 + 1));
-  for (int32_t j = 0; j < N / 2 + 1; ++j) {
-    twr[j] = cos(2.0 * PI * (double)j / (double)N);
-    twi[j] = (double)sign * sin(2.0 * PI * (double)j / (double)N);
-  }
-  const int64_t stride[3] = {1, N, (int64_t)N * N};
+void ibo_fft3(int32_t N1, int32_t N2, int32_t N3, double *re, double *im, int sign) {
+  const int32_t L[3] = {N1, N2, N3};
+  const int64_t stride[3] = {1, N1, (int64_t)N1 * N2};
   for (int ax = 0; ax < 3; ++ax) {
+    const int32_t N = L[ax];
     const int64_t s = stride[ax];
-    const int64_t s1 = stride[(ax + 1) % 3], s2 = stride[(ax + 2) % 3];
+    /* the two other axes enumerate the pencils */
+    const int a1 = (ax + 1) % 3, a2 = (ax + 2) % 3;
+    const int64_t s1 = stride[a1], s2 = stride[a2], n1 = L[a1], n2 = L[a2];
+    double *twr = (double *)malloc(sizeof(double) * (size_t)(N / 2 + 1));
+    double *twi = (double *)malloc(sizeof(double) * (size_t)(N / 2 + 1));
+    for (int32_t j = 0; j < N / 2 + 1; ++j) {
+      twr[j] = cos(2.0 * PI * (double)j / (double)N);
+      twi[j] = (double)sign * sin(2.0 * PI * (double)j / (double)N);
+    }
 #pragma omp parallel
     {
       double *pr = (double *)malloc(sizeof(double) * (size_t)N);
       double *pi = (double *)malloc(sizeof(double) * (size_t)N);
 #pragma omp for schedule(static)
-      for (int64_t pencil = 0; pencil < (int64_t)N * N; ++pencil) {
-        int64_t base = (pencil % N) * s1 + (pencil / N) * s2;
+      for (int64_t pencil = 0; pencil < n1 * n2; ++pencil) {
+        int64_t base = (pencil % n1) * s1 + (pencil / n1) * s2;
         for (int32_t j = 0; j < N; ++j) { pr[j] = re[base + j * s]; pi[j] = im[base + j * s]; }
         fft1(N, pr, pi, twr, twi);
         for (int32_t j = 0; j < N; ++j) { re[base + j * s] = pr[j]; im[base + j * s] = pi[j]; }
@@ -271,28 +276,17 @@ void ibo_fft3(int32_t N, double *re, double *im, int sign) {
       free(pr);
       free(pi);
     }
+    free(twr);
+    free(twi);
   }
-  free(twr);
-  free(twi);
 }
 
 /* Per-mode solve (DESIGN.md §2 S3c; readings Z6, Z7, Z22):
  *   d(k) = rho/dt + mu * sum_a 4 sin^2(pi k_a/N)/h^2      (symbol of -mu sum D+D-)
  *   s_a  = sin(2 pi k'_a/N)/h, exactly 0 when 2 k_a = 0 mod N   (D0 symbol = i s)
  *   p^   = -i (s.r^)/|s|^2,  u^ = (r^ - s (s.r^)/|s|^2)/d;   null modes: u^ = r^/d, p^ = 0. */
-void ibo_solve(int32_t N, double h, double rho, double mu, double dt, const double *r,
-               double *u_out, double *p_out) {
-  const int64_t V = (int64_t)N * N * N;
-  double *re = (double *)malloc(sizeof(double) * 3 * (size_t)V);
-  double *im = (double *)calloc(3 * (size_t)V, sizeof(double));
-  double *pre = p_out ? (double *)calloc((size_t)V, sizeof(double)) : NULL;
-  double *pim = p_out ? (double *)calloc((size_t)V, sizeof(double)) : NULL;
-  memcpy(re, r, sizeof(double) * 3 * (size_t)V);
-  for (int c = 0; c < 3; ++c) ibo_fft3(N, re + c * V, im + c * V, -1);
-
-  double *sk = (double *)malloc(sizeof(double) * (size_t)N);
-  double *lk = (double *)malloc(sizeof(double) * (size_t)N);
-  int *nul = (int *)malloc(sizeof(int) * (size_t)N);
+/* per-axis symbols of one lattice axis of length N (readings Z22) */
+static void axis_symbols(int32_t N, double h, double *sk, double *lk, int *nul) {
   for (int32_t k = 0; k < N; ++k) {
     int32_t ks = k > N / 2 ? k - N : k;                 /* signed frequency k' */
     nul[k] = (2 * k) % N == 0;                          /* decided on the integers */
@@ -300,16 +294,36 @@ void ibo_solve(int32_t N, double h, double rho, double mu, double dt, const doub
     double sn = sin(PI * (double)k / (double)N);
     lk[k] = 4.0 * sn * sn / (h * h);
   }
+}
+
+void ibo_solve(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu, double dt,
+               const double *r, double *u_out, double *p_out) {
+  const int64_t V = (int64_t)N1 * N2 * N3;
+  double *re = (double *)malloc(sizeof(double) * 3 * (size_t)V);
+  double *im = (double *)calloc(3 * (size_t)V, sizeof(double));
+  double *pre = p_out ? (double *)calloc((size_t)V, sizeof(double)) : NULL;
+  double *pim = p_out ? (double *)calloc((size_t)V, sizeof(double)) : NULL;
+  memcpy(re, r, sizeof(double) * 3 * (size_t)V);
+  for (int c = 0; c < 3; ++c) ibo_fft3(N1, N2, N3, re + c * V, im + c * V, -1);
+
+  double *sx = (double *)malloc(sizeof(double) * (size_t)N1), *lx = (double *)malloc(sizeof(double) * (size_t)N1);
+  double *sy = (double *)malloc(sizeof(double) * (size_t)N2), *ly = (double *)malloc(sizeof(double) * (size_t)N2);
+  double *sz = (double *)malloc(sizeof(double) * (size_t)N3), *lz = (double *)malloc(sizeof(double) * (size_t)N3);
+  int *nx = (int *)malloc(sizeof(int) * (size_t)N1), *ny = (int *)malloc(sizeof(int) * (size_t)N2);
+  int *nz = (int *)malloc(sizeof(int) * (size_t)N3);
+  axis_symbols(N1, h, sx, lx, nx);
+  axis_symbols(N2, h, sy, ly, ny);
+  axis_symbols(N3, h, sz, lz, nz);
 #pragma omp parallel for schedule(static)
-  for (int64_t kz = 0; kz < N; ++kz)
-    for (int64_t ky = 0; ky < N; ++ky)
-      for (int64_t kx = 0; kx < N; ++kx) {
-        const int64_t m = (kz * N + ky) * N + kx;
-        const double d = rho / dt + mu * (lk[kx] + lk[ky] + lk[kz]);
-        const double s[3] = {sk[kx], sk[ky], sk[kz]};
+  for (int64_t kz = 0; kz < N3; ++kz)
+    for (int64_t ky = 0; ky < N2; ++ky)
+      for (int64_t kx = 0; kx < N1; ++kx) {
+        const int64_t m = (kz * N2 + ky) * N1 + kx;
+        const double d = rho / dt + mu * (lx[kx] + ly[ky] + lz[kz]);
+        const double s[3] = {sx[kx], sy[ky], sz[kz]};
         double rr[3], ri[3];
         for (int c = 0; c < 3; ++c) { rr[c] = re[c * V + m]; ri[c] = im[c * V + m]; }
-        if (nul[kx] && nul[ky] && nul[kz]) {
+        if (nx[kx] && ny[ky] && nz[kz]) {
           for (int c = 0; c < 3; ++c) { re[c * V + m] = rr[c] / d; im[c * V + m] = ri[c] / d; }
           if (p_out) { pre[m] = 0.0; pim[m] = 0.0; }
           continue;
@@ -323,36 +337,36 @@ void ibo_solve(int32_t N, double h, double rho, double mu, double dt, const doub
         }
         if (p_out) { pre[m] = si / s2; pim[m] = -sr / s2; }   /* -i (sr + i si)/s2 */
       }
-  free(sk); free(lk); free(nul);
+  free(sx); free(lx); free(sy); free(ly); free(sz); free(lz); free(nx); free(ny); free(nz);
 
   const double inv = 1.0 / (double)V;
-  for (int c = 0; c < 3; ++c) ibo_fft3(N, re + c * V, im + c * V, +1);
+  for (int c = 0; c < 3; ++c) ibo_fft3(N1, N2, N3, re + c * V, im + c * V, +1);
   for (int64_t i = 0; i < 3 * V; ++i) u_out[i] = re[i] * inv;
   if (p_out) {
-    ibo_fft3(N, pre, pim, +1);
+    ibo_fft3(N1, N2, N3, pre, pim, +1);
     for (int64_t i = 0; i < V; ++i) p_out[i] = pre[i] * inv;
     free(pre); free(pim);
   }
   free(re); free(im);
 }
 
-void ibo_fluid_step(int32_t N, double h, double rho, double mu, double dt, const double *u,
-                    const double *F, double *u_out, double *p_out) {
-  const size_t V = (size_t)N * N * N;
+void ibo_fluid_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu,
+                    double dt, const double *u, const double *F, double *u_out, double *p_out) {
+  const size_t V = (size_t)N1 * N2 * N3;
   double *r = (double *)malloc(sizeof(double) * 3 * V);
-  ibo_rhs(N, h, rho, dt, u, F, r);
-  ibo_solve(N, h, rho, mu, dt, r, u_out, p_out);
+  ibo_rhs(N1, N2, N3, h, rho, dt, u, F, r);
+  ibo_solve(N1, N2, N3, h, rho, mu, dt, r, u_out, p_out);
   free(r);
 }
 
 /* ------------------------------------------------------------------ the time loop */
-int ibo_step(int32_t N, double h, double rho, double mu, double dt, double *u, double *p,
-             double *X, int64_t np, int32_t npatch, const int64_t *first, const int32_t *n1,
-             const int32_t *n2, const uint32_t *flags, const int64_t *param_off,
-             const double *stiff, int64_t nd, const int64_t *drive_idx,
-             const double *drive_dir, double drive_amp, int32_t drive_period, int64_t step0,
-             int32_t nsteps) {
-  const size_t V = (size_t)N * N * N;
+int ibo_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu, double dt,
+             double *u, double *p, double *X, int64_t np, int32_t npatch, const int64_t *first,
+             const int32_t *n1, const int32_t *n2, const uint32_t *flags,
+             const int64_t *param_off, const double *stiff, int64_t nd,
+             const int64_t *drive_idx, const double *drive_dir, double drive_amp,
+             int32_t drive_period, int64_t step0, int32_t nsteps, int32_t p_every) {
+  const size_t V = (size_t)N1 * N2 * N3;
   double *Fn = (double *)malloc(sizeof(double) * 3 * (size_t)(np > 0 ? np : 1));
   double *U = (double *)malloc(sizeof(double) * 3 * (size_t)(np > 0 ? np : 1));
   double *F = (double *)malloc(sizeof(double) * 3 * V);
@@ -362,9 +376,10 @@ int ibo_step(int32_t N, double h, double rho, double mu, double dt, double *u, d
     const int64_t n = step0 + s;
     ibo_force(X, np, npatch, first, n1, n2, flags, param_off, stiff, nd, drive_idx,
               drive_dir, drive_amp, drive_period, n, Fn);              /* step 1 */
-    ibo_spread(N, h, X, Fn, np, F);                                     /* step 2 */
-    ibo_fluid_step(N, h, rho, mu, dt, u, F, un, (s == nsteps - 1) ? p : NULL);  /* 3 */
-    ibo_interp(N, h, un, X, np, U);                                     /* step 4 */
+    ibo_spread(N1, N2, N3, h, X, Fn, np, F);                            /* step 2 */
+    double *ps = (p && (p_every || s == nsteps - 1)) ? p + (p_every ? (size_t)s * V : 0) : NULL;
+    ibo_fluid_step(N1, N2, N3, h, rho, mu, dt, u, F, un, ps);           /* step 3 */
+    ibo_interp(N1, N2, N3, h, un, X, np, U);                            /* step 4 */
     for (int64_t i = 0; i < 3 * np; ++i) X[i] = X[i] + dt * U[i];       /* eq:discreteX */
     memcpy(u, un, sizeof(double) * 3 * V);
     for (int64_t i = 0; i < 3 * np && !status; ++i) if (!isfinite(X[i])) status = 1 + s;

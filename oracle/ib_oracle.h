@@ -5,8 +5,8 @@
  * paper_math_0301321_b200/csrc); only tests/, __graft_entry__.smoke() and bench.py's
  * cpu_baseline / --impl reference legs may load it.
  *
- * Layouts: fields are [c][z][y][x] (x fastest), N^3 cells per component, lattice
- * x = h*(i,j,k); positions / nodal forces are [np][3].
+ * Layouts: fields are [c][z][y][x] (x fastest) on an N1 x N2 x N3 lattice (x, y, z),
+ * x = h*(i,j,k), periodic; positions / nodal forces are [np][3].
  * Structures are structured patches: point (i1,i2) of patch p is
  * first[p] + i2*n1[p] + i1; stiffness block layout as documented in gen/configs.py.
  */
@@ -41,43 +41,45 @@ void ibo_force(const double *X, int64_t np, int32_t npatch, const int64_t *first
 
 /* Step 2 — eq:discreteF: F = sum_q Fnode(q) delta_h(x - X(q)).
  * F[3][N^3] is overwritten.  Serial, point-index order. */
-void ibo_spread(int32_t N, double h, const double *X, const double *Fnode, int64_t np,
-                double *F);
+void ibo_spread(int32_t N1, int32_t N2, int32_t N3, double h, const double *X,
+                const double *Fnode, int64_t np, double *F);
 
 /* eq:discreteX interpolation: U(q) = sum_x u(x) delta_h(x-X(q)) h^3. */
-void ibo_interp(int32_t N, double h, const double *u, const double *X, int64_t np, double *U);
+void ibo_interp(int32_t N1, int32_t N2, int32_t N3, double h, const double *u, const double *X,
+                int64_t np, double *U);
 
 /* sum_k u_k^n D_k^{+-} u^n with the upwind rule of PAPER.md lines 676-691
  * (u_k = 0 -> backward difference, reading Z5).  adv[3][N^3]. */
-void ibo_advect(int32_t N, double h, const double *u, double *adv);
+void ibo_advect(int32_t N1, int32_t N2, int32_t N3, double h, const double *u, double *adv);
 
 /* Right-hand side of eq:discreteNS1 after moving u^{n+1}-free terms right:
  * r = rho u^n / dt - rho sum_k u_k D_k^{+-} u^n + F^n. */
-void ibo_rhs(int32_t N, double h, double rho, double dt, const double *u, const double *F,
-             double *r);
+void ibo_rhs(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double dt,
+             const double *u, const double *F, double *r);
 
-/* Unnormalised in-place 3-D complex DFT by radix-2 FFT along x, y, z.
- * sign = -1: X(k) = sum_j x(j) e^{-2 pi i k.j/N}; sign = +1: the conjugate kernel. */
-void ibo_fft3(int32_t N, double *re, double *im, int sign);
+/* Unnormalised in-place 3-D complex DFT by radix-2 FFT along x, y, z ([N3][N2][N1] arrays).
+ * sign = -1: X(k) = sum_j x(j) e^{-2 pi i sum_a k_a j_a / N_a}; sign = +1: the conjugate. */
+void ibo_fft3(int32_t N1, int32_t N2, int32_t N3, double *re, double *im, int sign);
 
 /* Solve eq:discreteNS1-2 for (u^{n+1}, p^{n+1}) given r.
  * u_out[3][N^3]; p_out[N^3] may be NULL. */
-void ibo_solve(int32_t N, double h, double rho, double mu, double dt, const double *r,
-               double *u_out, double *p_out);
+void ibo_solve(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu, double dt,
+               const double *r, double *u_out, double *p_out);
 
 /* Step 3: rhs + solve. */
-void ibo_fluid_step(int32_t N, double h, double rho, double mu, double dt, const double *u,
-                    const double *F, double *u_out, double *p_out);
+void ibo_fluid_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu,
+                    double dt, const double *u, const double *F, double *u_out, double *p_out);
 
-/* nsteps full IB steps.  u[3][N^3] and X[np][3] in/out; p (may be
- * NULL) receives p^{n+1} of the last step.  Returns 0, or 1 + the 0-based step index at
- * which a non-finite value appeared. */
-int ibo_step(int32_t N, double h, double rho, double mu, double dt, double *u, double *p,
-             double *X, int64_t np, int32_t npatch, const int64_t *first, const int32_t *n1,
-             const int32_t *n2, const uint32_t *flags, const int64_t *param_off,
-             const double *stiff, int64_t nd, const int64_t *drive_idx,
-             const double *drive_dir, double drive_amp, int32_t drive_period, int64_t step0,
-             int32_t nsteps);
+/* nsteps full IB steps.  u[3][V] and X[np][3] in/out; p (may be
+ * NULL) receives p^{n+1}: of the last step ([V]) when p_every == 0, of every step
+ * ([nsteps][V]) when p_every != 0.  Returns 0, or 1 + the 0-based step index at which a
+ * non-finite value appeared. */
+int ibo_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu, double dt,
+             double *u, double *p, double *X, int64_t np, int32_t npatch, const int64_t *first,
+             const int32_t *n1, const int32_t *n2, const uint32_t *flags,
+             const int64_t *param_off, const double *stiff, int64_t nd,
+             const int64_t *drive_idx, const double *drive_dir, double drive_amp,
+             int32_t drive_period, int64_t step0, int32_t nsteps, int32_t p_every);
 
 #ifdef __cplusplus
 }

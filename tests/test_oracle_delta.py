@@ -145,3 +145,25 @@ def test_interp_constants_linear_and_adjoint(olib):
     lhs = h ** 3 * np.sum(olib.spread(N, h, X, f) * v)
     rhs = np.sum(f * olib.interp(N, h, v, X))
     assert abs(lhs - rhs) <= 1e-12 * max(abs(lhs), 1.0)
+
+
+def test_spread_interp_anisotropic_conservation_and_adjoint(olib):
+    # on a 16 x 8 x 32 lattice: h^3 sum F = sum f, adjointness, constants reproduced,
+    # and periodic wrap on each axis with its own length
+    shape, h = (16, 8, 32), 1.0 / 16
+    rng = np.random.default_rng(21)
+    L = np.array(shape) * h
+    X = rng.uniform(-0.3, 1.3, (300, 3)) * L
+    f = rng.standard_normal((300, 3))
+    F = olib.spread(shape, h, X, f)
+    assert F.shape == (3, 32, 8, 16)
+    assert np.allclose(F.reshape(3, -1).sum(1) * h ** 3, f.sum(0), rtol=0, atol=1e-12 * np.abs(f).sum())
+    u = rng.standard_normal((3, 32, 8, 16))
+    U = olib.interp(shape, h, u, X)
+    assert abs(np.sum(F * u) * h ** 3 - np.sum(f * U)) <= 1e-12 * np.sum(np.abs(f * U))
+    c = np.ones((3, 32, 8, 16)) * np.array([0.3, -1.0, 2.0])[:, None, None, None]
+    assert np.allclose(olib.interp(shape, h, c, X), [0.3, -1.0, 2.0], rtol=0, atol=1e-14)
+    # a shift by the period N_a h along any axis changes nothing (to rounding of X + L)
+    for a in range(3):
+        Xs = X.copy(); Xs[:, a] += L[a]
+        assert np.allclose(olib.spread(shape, h, Xs, f), F, rtol=0, atol=1e-11 * np.abs(F).max())

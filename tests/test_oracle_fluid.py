@@ -191,3 +191,53 @@ def test_nyquist_null_space_integer_decision(olib):
     d = rho / dt + mu * 4 / h ** 2 * 1.0        # sin^2(pi (N/2)/N) = 1
     assert np.max(np.abs(u[0] - r[0] / d)) < 1e-15 * N
     assert np.max(np.abs(p)) == 0.0
+
+
+# ---------------------------------------------------------------- anisotropic lattices
+# (the paper's half-cube model is 256 x 256 x 128, PAPER.md 1003-1007)
+@pytest.mark.parametrize("shape", [(8, 4, 2), (4, 8, 16), (16, 2, 8)])
+def test_fft_equals_direct_dft_anisotropic(olib, shape):
+    n1, n2, n3 = shape
+    rng = np.random.default_rng(sum(shape))
+    x = rng.standard_normal((n3, n2, n1)) + 1j * rng.standard_normal((n3, n2, n1))
+
+    def W(n):
+        j = np.arange(n)
+        return np.exp(-2j * np.pi * np.outer(j, j) / n)
+    direct = np.einsum("az,by,cx,zyx->abc", W(n3), W(n2), W(n1), x)
+    got = olib.fft3(x, -1)
+    assert np.max(np.abs(got - direct)) < 1e-13 * np.max(np.abs(direct))
+
+
+@pytest.mark.parametrize("shape", [(8, 16, 4), (16, 8, 32)])
+def test_solve_physical_space_residual_anisotropic(olib, shape):
+    n1, n2, n3 = shape
+    h, rho, mu, dt = 1.0 / 16, 1.1, 0.03, 1e-2
+    r = np.random.default_rng(13).standard_normal((3, n3, n2, n1))
+    u, p = olib.solve(shape, h, rho, mu, dt, r)
+    gp = np.stack([D0(p, a, h) for a in range(3)])
+    res = rho * u / dt + gp - mu * np.stack([lap(u[a], h) for a in range(3)]) - r
+    assert np.max(np.abs(res)) < 1e-12 * np.max(np.abs(r))
+    assert np.max(np.abs(div0(u, h))) < 1e-12 * np.max(np.abs(u)) / h
+
+
+@pytest.mark.parametrize("axis", [0, 1, 2])
+def test_single_mode_decay_anisotropic(olib, axis):
+    # u_c = A sin(2 pi m j_a / N_a) along axis a (c != a): advection and projection vanish;
+    # u^n = A (1 + mu dt (4/h^2) sin^2(pi m/N_a)/rho)^-n
+    shape = (16, 8, 32)
+    h, rho, mu, dt, A, m = 1.0 / 16, 1.0, 0.02, 1e-3, 0.5, 3
+    n = shape[axis]
+    j = np.arange(n)
+    prof = A * np.sin(2 * np.pi * m * j / n)
+    bshape = [1, 1, 1]
+    bshape[2 - axis] = n
+    u = np.zeros((3, shape[2], shape[1], shape[0]))
+    c = (axis + 1) % 3
+    u[c] = prof.reshape(bshape)
+    F = np.zeros_like(u)
+    g = 1.0 / (1.0 + mu * dt * 4.0 / h ** 2 * np.sin(np.pi * m / n) ** 2 / rho)
+    for k in range(1, 4):
+        u, _ = olib.fluid_step(shape, h, rho, mu, dt, u, F)
+        assert np.max(np.abs(u[c] - g ** k * prof.reshape(bshape))) <= 1e-10 * A * g ** k
+        assert np.max(np.abs(u[(c + 1) % 3])) == 0.0 and np.max(np.abs(u[(c + 2) % 3])) == 0.0
