@@ -115,17 +115,28 @@ class _Builder:
 
 
 # --------------------------------------------------------------------------- velocity
-def random_divfree_velocity(N: int, K: int, amplitude: float, rng: np.random.Generator) -> np.ndarray:
+def _dims(N):
+    """(N1, N2, N3) from an int (cubic lattice) or a 3-sequence (x, y, z)."""
+    if isinstance(N, (tuple, list)):
+        return tuple(int(v) for v in N)
+    return int(N), int(N), int(N)
+
+
+def random_divfree_velocity(N, K: int, amplitude: float, rng: np.random.Generator,
+                            h: float = None) -> np.ndarray:
     """Seeded random discretely divergence-free field (reading Z19).
 
     A vector potential A with random Fourier coefficients on the modes 0 < |k|^2 <= K^2
     (half-space representatives, loops k1, k2, k3 from -K to K, k3 outermost) is evaluated
     on the grid; u = D0 x A (centred-difference curl) so that D0 . u = 0 up to rounding;
     u is then scaled so that its RMS speed sqrt(mean |u|^2) equals `amplitude`.
-    Returns [3][N][N][N] (component, z, y, x), x fastest.
+    N is an int (N^3 lattice) or (N1, N2, N3); h defaults to 1/N1.
+    Returns [3][N3][N2][N1] (component, z, y, x), x fastest.
     """
-    spec = np.zeros((3, N, N, N // 2 + 1), dtype=np.complex128)
-    scale = N ** 3 / 2.0
+    n1, n2, n3 = _dims(N)
+    h = 1.0 / n1 if h is None else h
+    spec = np.zeros((3, n3, n2, n1 // 2 + 1), dtype=np.complex128)
+    scale = n1 * n2 * n3 / 2.0
     for k3 in range(-K, K + 1):
         for k2 in range(-K, K + 1):
             for k1 in range(-K, K + 1):
@@ -137,14 +148,14 @@ def random_divfree_velocity(N: int, K: int, amplitude: float, rng: np.random.Gen
                 b = rng.standard_normal(3)
                 c = (a - 1j * b) * scale          # Re(c e^{i theta}) = a cos + b sin
                 if k1 > 0:
-                    spec[:, k3 % N, k2 % N, k1] += c
+                    spec[:, k3 % n3, k2 % n2, k1] += c
                 elif k1 < 0:
-                    spec[:, (-k3) % N, (-k2) % N, -k1] += np.conj(c)
+                    spec[:, (-k3) % n3, (-k2) % n2, -k1] += np.conj(c)
                 else:
-                    spec[:, k3 % N, k2 % N, 0] += c
-                    spec[:, (-k3) % N, (-k2) % N, 0] += np.conj(c)
-    A = np.fft.irfftn(spec, s=(N, N, N), axes=(1, 2, 3))   # A[c][z][y][x]
-    inv2h = N / 2.0   # 1/(2h), h = 1/N
+                    spec[:, k3 % n3, k2 % n2, 0] += c
+                    spec[:, (-k3) % n3, (-k2) % n2, 0] += np.conj(c)
+    A = np.fft.irfftn(spec, s=(n3, n2, n1), axes=(1, 2, 3))   # A[c][z][y][x]
+    inv2h = 1.0 / (2.0 * h)
 
     def d0(f, ax):   # ax: 0 = x, 1 = y, 2 = z on a [z][y][x] array
         a = {0: 2, 1: 1, 2: 0}[ax]
@@ -337,14 +348,15 @@ def random_points(n: int, rng: np.random.Generator, lo: float = 0.0, hi: float =
     return np.ascontiguousarray(rng.uniform(lo, hi, size=(n, 3)))
 
 
-def small_sheet_config(N: int = 16, n1: int = 12, n2: int = 10, seed: int = 0,
+def small_sheet_config(N=16, n1: int = 12, n2: int = 10, seed: int = 0,
                        flags: int = STRETCH1 | STRETCH2 | BEND1 | BEND2,
                        tether: bool = True, drive: bool = True, u_amp: float = 0.0,
                        rho: float = 1.0, mu: float = 0.01, dt: float = 1e-3,
                        spacing: float = None, noise: float = 0.3) -> Config:
-    """A small stressed sheet (+ optional tethered patch and drive) for parity tests."""
+    """A small stressed sheet (+ optional tethered patch and drive) for parity tests.
+    N is an int or (N1, N2, N3); h = 1/N1 (the domain is [0, N1 h) x [0, N2 h) x [0, N3 h))."""
     rng = np.random.default_rng(seed)
-    h = 1.0 / N
+    h = 1.0 / _dims(N)[0]
     s = h / 2 if spacing is None else spacing
     i1 = np.arange(n1, dtype=np.float64)[None, :]
     i2 = np.arange(n2, dtype=np.float64)[:, None]
@@ -370,7 +382,8 @@ def small_sheet_config(N: int = 16, n1: int = 12, n2: int = 10, seed: int = 0,
         b.add(T, TETHER, [rng.uniform(10.0, 50.0, m1 * m2), Y])
     X, S = b.arrays()
     u0 = random_divfree_velocity(N, 3, u_amp, rng) if u_amp > 0 else None
-    cfg = Config(f"sheet{N}", N, h, rho, mu, dt, 10, X, b.patches, S, u0=u0)
+    name = "sheet" + ("x".join(str(v) for v in N) if isinstance(N, (tuple, list)) else str(N))
+    cfg = Config(name, N, h, rho, mu, dt, 10, X, b.patches, S, u0=u0)
     if drive:
         cfg.drive_idx = np.arange(0, n1, 3, dtype=np.int64)
         d = rng.standard_normal((cfg.drive_idx.size, 3))

@@ -7,14 +7,15 @@
  *   3. the upwind / implicit-viscosity Navier-Stokes system solved by FFT
  *                                                                (eq:discreteNS1-2, 659-695)
  *   4. X^{n+1} = X^n + dt sum_x u^{n+1}(x) delta_h(x - X^n) h^3  (eq:discreteX, 725-734)
- * with Peskin's 4-point delta_h (745-759) on a periodic N^3 lattice x = h(i,j,k).
+ * with Peskin's 4-point delta_h (745-759) on a periodic N1 x N2 x N3 lattice x = h(i,j,k).
  *
  * Conventions (all calls):
  *  - every floating-point array is fp64;
  *  - every pointer argument may be HOST or DEVICE memory (CUDA unified addressing decides);
  *    the library copies in/out synchronously on the context's stream and keeps no
  *    reference to caller memory after the call returns; the caller owns all its buffers;
- *  - fields are SoA [3][N][N][N] = [component][z][y][x], x fastest; p is [N][N][N];
+ *  - fields are SoA [3][N3][N2][N1] = [component][z][y][x], x fastest (N1 = N2 = N3 = N for
+ *    ib_create); p is [N3][N2][N1];
  *  - positions and nodal forces are AoS [np][3]; positions are unwrapped (indices mod N);
  *  - one ctx = one state = one CUDA stream; calls on one ctx must be externally
  *    serialised; the library owns all device memory of a ctx;
@@ -76,6 +77,13 @@ enum {
  * Rejects: N not a power of two or N < 8 or N > 512; h <= 0; rho <= 0; mu < 0; dt <= 0.
  * The fluid starts at rest, no structure, step counter n = 0.  NULL on error. */
 ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt);
+/* The same on an anisotropic N1 x N2 x N3 lattice (x, y, z) of mesh width h, domain
+ * [0, N1 h) x [0, N2 h) x [0, N3 h) — e.g. the paper's 256 x 256 x 128 half-cube model
+ * (PAPER.md 1003-1007).  Fields are then [3][N3][N2][N1] (x fastest), p is [N3][N2][N1].
+ * Rejects, besides the ib_create cases per axis: N2 not a multiple of the x-pass row
+ * block (64 / max(1, N1/32), at most N1: 8 for N1 = 256, 4 for 512). */
+ib_ctx *ib_create3(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu,
+                   double dt);
 void ib_destroy(ib_ctx *ctx);
 
 /* Run all work of ctx on this CUDA stream (a cudaStream_t, e.g. torch's current stream);
@@ -90,7 +98,7 @@ int ib_set_structure(ib_ctx *ctx, const double *points, int64_t np, const ib_pat
                      int32_t npatch, const double *stiffness, int64_t nstiff);
 /* Replace positions only ([np][3], same np as the structure). */
 int ib_set_positions(ib_ctx *ctx, const double *points);
-/* Fluid velocity u^n, [3][N][N][N]. */
+/* Fluid velocity u^n, [3][N3][N2][N1]. */
 int ib_set_velocity(ib_ctx *ctx, const double *u);
 /* External drive (PAPER.md 988-993, simplified): F_idx[d] += amp * sin(2 pi n / period) *
  * dir[d] at step n (t^n = n dt).  n = 0 clears the drive. */
@@ -101,7 +109,7 @@ int ib_set_drive(ib_ctx *ctx, const int64_t *idx, int64_t n, const double *dir,
  * (ib_last_error names the step) if u or X became non-finite. */
 int ib_step(ib_ctx *ctx, int32_t nsteps);
 
-/* Copy out u^n ([3][N^3], may be NULL) and p^n ([N^3], may be NULL; needs
+/* Copy out u^n ([3][V], V = N1 N2 N3, may be NULL) and p^n ([V], may be NULL; needs
  * IB_OPT_PRESSURE enabled before the last ib_step, else IB_ESTATE). */
 int ib_get_fields(ib_ctx *ctx, double *u, double *p);
 int ib_get_positions(ib_ctx *ctx, double *X);
@@ -129,8 +137,8 @@ int ib_debug_rhs(ib_ctx *ctx, const double *u, const double *F, double *r_out);
 /* u^{n+1}, p^{n+1} from (u^n, F^n): the fluid part of the step (p_out may be NULL). */
 int ib_debug_fluid(ib_ctx *ctx, const double *u, const double *F, double *u_out,
                    double *p_out);
-/* Forward 3-D real-to-complex DFT of a real field [N^3] (unnormalised, e^{-2 pi i k.j/N}):
- * out = complex half spectrum [N][N][N/2+1] as interleaved (re, im). */
+/* Forward 3-D real-to-complex DFT of a real field [V] (unnormalised, e^{-2 pi i sum k_a j_a/N_a}):
+ * out = complex half spectrum [N3][N2][N1/2+1] as interleaved (re, im). */
 int ib_debug_fft(ib_ctx *ctx, const double *in, double *out);
 
 #ifdef __cplusplus

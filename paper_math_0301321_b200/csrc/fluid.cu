@@ -51,6 +51,8 @@ __device__ __forceinline__ long long step_of(const long long *dev_n, long long n
 }
 
 // ------------------------------------------------------------------ tables
+// Per-axis tables of a lattice axis of length N: twiddles exp(-2 pi i t/N), the D0 symbol
+// s and -symbol of D+D- l; twM (x axis only, may be null): exp(-2 pi i t/M), M = N/2.
 __global__ void k_init_tables(double2 *twN, int N, double2 *twM, int M, double *s, double *l,
                               double h) {
   int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -64,7 +66,7 @@ __global__ void k_init_tables(double2 *twN, int N, double2 *twM, int M, double *
     const double sh = sinpi((double)t / (double)N);
     l[t] = 4.0 * sh * sh / (h * h);                       // -symbol of D+D-
   }
-  if (t < M) {
+  if (twM && t < M) {
     double sn, cs;
     sincospi(2.0 * (double)t / (double)M, &sn, &cs);
     twM[t] = make_double2(cs, -sn);
@@ -72,10 +74,12 @@ __global__ void k_init_tables(double2 *twN, int N, double2 *twM, int M, double *
 }
 
 cudaError_t init_tables(ib_ctx *c) {
-  const int N = c->g.N;
-  k_init_tables<<<(N + 127) / 128, 128, 0, c->stream>>>(c->twN, N, c->twM, N / 2, c->sym_s,
-                                                        c->sym_l, c->g.h);
-  c->launches++;
+  const int L[3] = {c->g.N1, c->g.N2, c->g.N3};
+  for (int a = 0; a < 3; ++a) {
+    k_init_tables<<<(L[a] + 127) / 128, 128, 0, c->stream>>>(
+        c->tw[a], L[a], a == 0 ? c->twM : nullptr, L[0] / 2, c->sym_s[a], c->sym_l[a], c->g.h);
+    c->launches++;
+  }
   return cudaGetLastError();
 }
 
@@ -99,12 +103,13 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   __shared__ uint64_t tbar;
   // 128-byte aligned tile (TMA destination); offset arithmetic keeps accesses LDS/STS
   double2 *sm = smraw_x + ((128u - (smem_u32(smraw_x) & 127u)) & 127u) / 16u;
-  double *ut = reinterpret_cast<double *>(sm);     // u tile [comp][UR][N]
+  double *ut = reinterpret_cast<double *>(sm);     // u tile [comp][UR][N1]
+  const int N2 = g.N2, N3 = g.N3;                  // rows per plane, planes
   const int z = blockIdx.y, y0 = blockIdx.x * RB;
   const int t = threadIdx.x % T, pencil = threadIdx.x / T;
   const int row = pencil % RB, comp = pencil / RB, y = y0 + row;
-  const size_t V = (size_t)N * N * N;
-  const size_t rowbase = ((size_t)z * N + y) * N;
+  const size_t V = (size_t)g.V;
+  const size_t rowbase = ((size_t)z * N2 + y) * N;
   const double cu = g.rho / g.dt, ra = g.rho * g.invh;
   if (MODE != 2 && use_tma) {   // one thread streams the 3 x (RB + 2) rows with TMA
     if (threadIdx.x == 0) {
@@ -112,10 +117,10 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
       fence_mbar_init();
       mbar_expect_tx(&tbar, (uint32_t)(3 * UR * N * 8));
       for (int c = 0; c < 3; ++c) {
-        const int rb = (c * N + z) * N;
+        const int rb = (c * N3 + z) * N2;
         tma_load_2d(ut + ((size_t)c * UR + 1) * N, &map_rows, 0, rb + y0, &tbar);
-        tma_load_2d(ut + (size_t)c * UR * N, &map_row1, 0, rb + ((y0 - 1 + N) & (N - 1)), &tbar);
-        tma_load_2d(ut + ((size_t)c * UR + RB + 1) * N, &map_row1, 0, rb + ((y0 + RB) & (N - 1)), &tbar);
+        tma_load_2d(ut + (size_t)c * UR * N, &map_row1, 0, rb + ((y0 - 1 + N2) & (N2 - 1)), &tbar);
+        tma_load_2d(ut + ((size_t)c * UR + RB + 1) * N, &map_row1, 0, rb + ((y0 + RB) & (N2 - 1)), &tbar);
       }
     }
     __syncthreads();                                // barrier initialised before anyone waits
@@ -124,18 +129,18 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
     constexpr int CH = N / 2;                      // 16-byte chunks per row
     for (int idx = threadIdx.x; idx < 3 * UR * CH; idx += blockDim.x) {
       const int ch = idx % CH, rr = (idx / CH) % UR, cc = idx / (CH * UR);
-      const int yy = (y0 - 1 + rr + N) & (N - 1);
+      const int yy = (y0 - 1 + rr + N2) & (N2 - 1);
       cp_async16(ut + ((size_t)cc * UR + rr) * N + 2 * ch,
-                 u + cc * V + ((size_t)z * N + yy) * N + 2 * ch, true);
+                 u + cc * V + ((size_t)z * N2 + yy) * N + 2 * ch, true);
     }
     cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
   }
   // F is only read on rows the spread touched (row flags), else taken as 0
-  const bool hasF = MODE == 1 || (MODE == 0 && (rowflag == nullptr || rowflag[(size_t)z * N + y] != 0));
-  const size_t zm = ((size_t)((z + N - 1) & (N - 1)) * N + y) * N;
-  const size_t zp = ((size_t)((z + 1) & (N - 1)) * N + y) * N;
+  const bool hasF = MODE == 1 || (MODE == 0 && (rowflag == nullptr || rowflag[(size_t)z * N2 + y] != 0));
+  const size_t zm = ((size_t)((z + N3 - 1) & (N3 - 1)) * N2 + y) * N;
+  const size_t zp = ((size_t)((z + 1) & (N3 - 1)) * N2 + y) * N;
   const double *uc_ = u + (MODE == 2 ? 0 : comp * V);
   const double *own = ut + ((size_t)comp * UR + row + 1) * N;        // this row, own comp
 
@@ -185,7 +190,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   auto bar = []() { __syncthreads(); };             // u tile dead before pencils alias it
   fft_io<M, -1, false, true>(sp, t, twM, ld, sst, bar);
   __syncthreads();
-  if (MODE == 0 && rowflag && threadIdx.x < RB) rowflag[(size_t)z * N + y0 + threadIdx.x] = 0u;
+  if (MODE == 0 && rowflag && threadIdx.x < RB) rowflag[(size_t)z * N2 + y0 + threadIdx.x] = 0u;
   // split the length-M transform Z of z_n = r_2n + i r_2n+1 into X_k, k = 0..M:
   // E = (Z_k + conj Z_{M-k})/2, O = -i (Z_k - conj Z_{M-k})/2, X_k = E + w^k O,
   // X_{M-k} = conj(E - w^k O), w = exp(-2 pi i/N).
@@ -198,7 +203,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
     const double2 E = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
     const double2 O = make_double2(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
     const double2 wO = cmul(__ldg(&twN[k]), O);
-    double2 *out = spec + (((size_t)cp * N + z) * N + (y0 + rw)) * g.P;
+    double2 *out = spec + (((size_t)cp * N3 + z) * N2 + (y0 + rw)) * g.P;
     out[k] = cadd(E, wO);
     if (k != M - k) out[M - k] = cconj(csub(E, wO));
   }
@@ -210,7 +215,8 @@ static cudaError_t launch_xfwd_n(const FluidGeom &g, int mode, const double *u, 
                                  double2 *spec, const double2 *twN, const double2 *twM,
                                  const XMapsU *um, cudaStream_t s) {
   using X = XCfg<N>;
-  dim3 grid(N / X::RB, N);
+  if (g.N2 % X::RB) return cudaErrorInvalidValue;     // ib_create3 checks this
+  dim3 grid(g.N2 / X::RB, g.N3);
   const int nc = mode == 2 ? 1 : 3;
   const size_t fft = (size_t)nc * X::RB * Plan<N / 2>::LD * sizeof(double2);
   const size_t tile = mode == 2 ? 0 : (size_t)3 * (X::RB + 2) * N * sizeof(double);
@@ -243,17 +249,18 @@ template <int N, int SIGN>
 __global__ void __launch_bounds__(YCfg<N>::C * YCfg<N>::T)
 k_ypass(FluidGeom g, const double2 *in, double2 *out, size_t in_zs, size_t in_es,
         size_t out_zs, size_t out_es, int ncomp, const double2 *__restrict__ twN) {
-  constexpr int C = YCfg<N>::C, LD = Plan<N>::LD, M = N / 2, NT = C * Plan<N>::T;
+  constexpr int C = YCfg<N>::C, LD = Plan<N>::LD, NT = C * Plan<N>::T;
+  const int M = g.M, N3 = g.N3;                     // kx in [0, M]; z planes
   extern __shared__ double2 sm[];
   double2 *pf = sm + C * LD;              // prefetch slots [PF_DEPTH][RMAX][NT]
   constexpr int SLOTS = Plan<N>::RMAX * NT;
   const int col = threadIdx.x % C, t = threadIdx.x / C;
-  constexpr int NBLK = (M + 1 + C - 1) / C;
-  const int ntiles = NBLK * N * ncomp;
-  const size_t cstride = (size_t)N * N * g.P;
+  const int NBLK = (M + 1 + C - 1) / C;
+  const int ntiles = NBLK * N3 * ncomp;
+  const size_t cstride = (size_t)N * N3 * g.P;
   auto prefetch = [&](int tile, int stage) {
     if (tile < ntiles) {
-      const int kx = (tile % NBLK) * C + col, z = (tile / NBLK) % N, comp = tile / (NBLK * N);
+      const int kx = (tile % NBLK) * C + col, z = (tile / NBLK) % N3, comp = tile / (NBLK * N3);
       const bool ok = kx <= M;
       const double2 *ib = in + comp * cstride + z * in_zs + (ok ? kx : 0);
       double2 *dst = pf + stage * SLOTS + threadIdx.x;
@@ -265,7 +272,7 @@ k_ypass(FluidGeom g, const double2 *in, double2 *out, size_t in_zs, size_t in_es
   for (int d = 0; d < PF_DEPTH; ++d) prefetch(blockIdx.x + d * gridDim.x, d);
   int stage = 0;
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int kx = (tile % NBLK) * C + col, z = (tile / NBLK) % N, comp = tile / (NBLK * N);
+    const int kx = (tile % NBLK) * C + col, z = (tile / NBLK) % N3, comp = tile / (NBLK * N3);
     const bool ok = kx <= M;
     double2 *ob = out + comp * cstride + z * out_zs + kx;
     cp_async_wait<PF_DEPTH - 1>();
@@ -300,10 +307,12 @@ static cudaError_t launch_ypass_n(const FluidGeom &g, int sign, const double2 *i
   using Y = YCfg<N>;
   const int threads = Y::C * Y::T;
   const size_t smem = ((size_t)Y::C * Plan<N>::LD + (size_t)PF_DEPTH * Plan<N>::RMAX * threads) * sizeof(double2);
-  const int ntiles = ((N / 2 + 1 + Y::C - 1) / Y::C) * N * ncomp;
-  const size_t P = g.P, NP = (size_t)N * g.P;
-  const size_t izs = in_layout == 1 ? NP : P, ies = in_layout == 1 ? P : NP;
-  const size_t ozs = out_layout == 1 ? NP : P, oes = out_layout == 1 ? P : NP;
+  const int ntiles = ((g.M + 1 + Y::C - 1) / Y::C) * g.N3 * ncomp;
+  // S1 [comp][z][y][kx]: z stride N2 P, y stride P; S2 [comp][ky][z][kx]: z stride P,
+  // ky stride N3 P  (N = N2 here)
+  const size_t P = g.P, N2P = (size_t)N * g.P, N3P = (size_t)g.N3 * g.P;
+  const size_t izs = in_layout == 1 ? N2P : P, ies = in_layout == 1 ? P : N3P;
+  const size_t ozs = out_layout == 1 ? N2P : P, oes = out_layout == 1 ? P : N3P;
   if (sign < 0) {
     const int grid = persistent_grid(k_ypass<N, -1>, threads, smem, ntiles);
     k_ypass<N, -1><<<grid, threads, smem, s>>>(g, in, out, izs, ies, ozs, oes, ncomp, twN);
@@ -324,23 +333,23 @@ static cudaError_t launch_ypass_n(const FluidGeom &g, int sign, const double2 *i
 // in smem; inverse FFT: smem -> registers -> smem exchange -> HBM.
 template <int N, int MODE, bool PRESS>
 __global__ void __launch_bounds__((PRESS ? 4 : 3) * ZCfg<N>::C * ZCfg<N>::T, PRESS ? 1 : ZCfg<N>::MINB)
-k_zpass(FluidGeom g, double2 *spec, double2 *pspec, const double2 *__restrict__ twN,
-        const double *__restrict__ sym_s, const double *__restrict__ sym_l) {
-  constexpr int C = ZCfg<N>::C, T = ZCfg<N>::T, LD = Plan<N>::LD, M = N / 2;
+k_zpass(FluidGeom g, double2 *spec, double2 *pspec, const double2 *__restrict__ twN, Sym sym) {
+  constexpr int C = ZCfg<N>::C, T = ZCfg<N>::T, LD = Plan<N>::LD;
   constexpr int NG = PRESS ? 4 : 3, NT = NG * C * T;
-  constexpr int NBLK = (M + 1 + C - 1) / C;
+  const int M = g.M, N2 = g.N2;                     // kx in [0, M]; ky in [0, N2)
+  const int NBLK = (M + 1 + C - 1) / C;
   extern __shared__ double2 sm[];
   double2 *pf = sm + NG * C * LD;         // prefetch slots [PF_DEPTH][RMAX][NT]
   constexpr int SLOTS = Plan<N>::RMAX * NT;
   const int t = threadIdx.x % T, col = (threadIdx.x / T) % C, grp = threadIdx.x / (C * T);
-  const int ntiles = NBLK * N;
+  const int ntiles = NBLK * N2;
   const size_t zs = g.P;                           // S2 layout: [comp][ky][z][kx]
   double2 *sp = sm + (grp * C + col) * LD;
   auto prefetch = [&](int tile, int stage) {
     if (tile < ntiles) {
       const int kx = (tile % NBLK) * C + col, ky = tile / NBLK;
       const bool ok = kx <= M && grp < 3;
-      const double2 *b = spec + ((size_t)(grp < 3 ? grp : 0) * N + ky) * N * g.P + (ok ? kx : 0);
+      const double2 *b = spec + ((size_t)(grp < 3 ? grp : 0) * N2 + ky) * N * g.P + (ok ? kx : 0);
       double2 *dst = pf + stage * SLOTS + threadIdx.x;
       pass0_foreach<N>(t, [&](int slot, int e) { cp_async16(dst + slot * NT, b + e * zs, ok); });
     }
@@ -352,7 +361,7 @@ k_zpass(FluidGeom g, double2 *spec, double2 *pspec, const double2 *__restrict__ 
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int col0 = (tile % NBLK) * C, ky = tile / NBLK, kx = col0 + col;
     const bool ok = kx <= M;
-    double2 *base = grp < 3 ? spec + ((size_t)grp * N + ky) * N * g.P + kx
+    double2 *base = grp < 3 ? spec + ((size_t)grp * N2 + ky) * N * g.P + kx
                             : pspec + (size_t)ky * N * g.P + kx;
     auto gst = [&](int e, double2 v) { if (ok) base[e * zs] = v; };
     auto sst = [sp](int e, double2 v) { sp[PAD(e)] = v; };
@@ -371,19 +380,19 @@ k_zpass(FluidGeom g, double2 *spec, double2 *pspec, const double2 *__restrict__ 
     fft_io<N, -1, false, true>(sp, t, twN, ld, sst, nxt);
     __syncthreads();
     {
-      const double sy = sym_s[ky], ly = sym_l[ky];
-      const bool ny = (ky == 0) || (ky == M);
-      const double invV = 1.0 / ((double)N * (double)N * (double)N);
+      const double sy = sym.sy[ky], ly = sym.ly[ky];
+      const bool ny = (ky == 0) || (2 * ky == N2);
+      const double invV = 1.0 / (double)g.V;
       for (int idx = threadIdx.x; idx < C * N; idx += blockDim.x) {
         const int c = idx / N, kz = idx % N, kxx = col0 + c;
         if (kxx > M) continue;
-        const double sx = sym_s[kxx], sz = sym_s[kz];
-        const double d = g.rho / g.dt + g.mu * (sym_l[kxx] + ly + sym_l[kz]);
+        const double sx = sym.sx[kxx], sz = sym.sz[kz];
+        const double d = g.rho / g.dt + g.mu * (sym.lx[kxx] + ly + sym.lz[kz]);
         double2 *q0 = sm + (0 * C + c) * LD + PAD(kz);
         double2 *q1 = q0 + C * LD;
         double2 *q2 = q1 + C * LD;
         const double2 r0 = *q0, r1 = *q1, r2 = *q2;
-        const bool nul = ny && (kxx == 0 || kxx == M) && (kz == 0 || kz == M);
+        const bool nul = ny && (kxx == 0 || kxx == M) && (kz == 0 || 2 * kz == N);
         if (nul) {
           const double inv = invV / d;
           *q0 = cscale(r0, inv); *q1 = cscale(r1, inv); *q2 = cscale(r2, inv);
@@ -410,22 +419,21 @@ k_zpass(FluidGeom g, double2 *spec, double2 *pspec, const double2 *__restrict__ 
 
 template <int N>
 static cudaError_t launch_zpass_n(const FluidGeom &g, int mode, double2 *spec, double2 *pspec,
-                                  const double2 *twN, const double *s_, const double *l_,
-                                  cudaStream_t s) {
+                                  const double2 *twN, const Sym &sym, cudaStream_t s) {
   using Z = ZCfg<N>;
-  const int ntiles = ((N / 2 + 1 + Z::C - 1) / Z::C) * N;
+  const int ntiles = ((g.M + 1 + Z::C - 1) / Z::C) * g.N2;
   const int t3 = 3 * Z::C * Z::T, t4 = 4 * Z::C * Z::T;
   const size_t smem3 = ((size_t)3 * Z::C * Plan<N>::LD + (size_t)PF_DEPTH * Plan<N>::RMAX * t3) * sizeof(double2);
   const size_t smem4 = ((size_t)4 * Z::C * Plan<N>::LD + (size_t)PF_DEPTH * Plan<N>::RMAX * t4) * sizeof(double2);
   if (mode == 1) {
     const int grid = persistent_grid(k_zpass<N, 1, false>, t3, smem3, ntiles);
-    k_zpass<N, 1, false><<<grid, t3, smem3, s>>>(g, spec, pspec, twN, s_, l_);
+    k_zpass<N, 1, false><<<grid, t3, smem3, s>>>(g, spec, pspec, twN, sym);
   } else if (pspec) {
     const int grid = persistent_grid(k_zpass<N, 0, true>, t4, smem4, ntiles);
-    k_zpass<N, 0, true><<<grid, t4, smem4, s>>>(g, spec, pspec, twN, s_, l_);
+    k_zpass<N, 0, true><<<grid, t4, smem4, s>>>(g, spec, pspec, twN, sym);
   } else {
     const int grid = persistent_grid(k_zpass<N, 0, false>, t3, smem3, ntiles);
-    k_zpass<N, 0, false><<<grid, t3, smem3, s>>>(g, spec, pspec, twN, s_, l_);
+    k_zpass<N, 0, false><<<grid, t3, smem3, s>>>(g, spec, pspec, twN, sym);
   }
   return cudaGetLastError();
 }
@@ -444,9 +452,9 @@ k_xinv(FluidGeom g, const double2 *__restrict__ spec, double *out, int ncomp,
   const int z = blockIdx.y, y0 = blockIdx.x * RB;
   const int t = threadIdx.x % T, pencil = threadIdx.x / T;
   const int row = pencil % RB, comp = pencil / RB;
-  const double2 *in = spec + (((size_t)comp * N + z) * N + (y0 + row)) * g.P;
-  const size_t V = (size_t)N * N * N;
-  double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * N + (y0 + row)) * N);
+  const double2 *in = spec + (((size_t)comp * g.N3 + z) * g.N2 + (y0 + row)) * g.P;
+  const size_t V = (size_t)g.V;
+  double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * g.N2 + (y0 + row)) * N);
   auto ld = [&](int e) -> double2 {
     double2 Xk = in[e], Xm = in[M - e];
     if (e == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real
@@ -473,7 +481,8 @@ static cudaError_t launch_xinv_n(const FluidGeom &g, const double2 *spec, double
                                  long long *flag, const long long *dev_n, long long n,
                                  cudaStream_t s) {
   using X = XCfg<N>;
-  dim3 grid(N / X::RB, N);
+  if (g.N2 % X::RB) return cudaErrorInvalidValue;
+  dim3 grid(g.N2 / X::RB, g.N3);
   const size_t smem = (size_t)ncomp * X::RB * Plan<N / 2>::LD * sizeof(double2);
   k_xinv<N><<<grid, ncomp * X::RB * X::T, smem, s>>>(g, spec, out, ncomp, twN, twM, flag,
                                                      dev_n, n);
@@ -498,7 +507,7 @@ cudaError_t launch_xfwd(const FluidGeom &g, int mode, const double *u, double *F
                         const double2 *twN, const double2 *twM, const XMapsU *um,
                         cudaStream_t s) {
 #define CALL(n) launch_xfwd_n<n>(g, mode, u, F, rowflag, in, r_out, spec, twN, twM, um, s)
-  IBK_DISPATCH_N(g.N, CALL)
+  IBK_DISPATCH_N(g.N1, CALL)
 #undef CALL
 }
 
@@ -506,15 +515,14 @@ cudaError_t launch_ypass(const FluidGeom &g, int sign, const double2 *in, int in
                          double2 *out, int out_layout, int ncomp, const double2 *twN,
                          cudaStream_t s) {
 #define CALL(n) launch_ypass_n<n>(g, sign, in, in_layout, out, out_layout, ncomp, twN, s)
-  IBK_DISPATCH_N(g.N, CALL)
+  IBK_DISPATCH_N(g.N2, CALL)
 #undef CALL
 }
 
 cudaError_t launch_zpass(const FluidGeom &g, int mode, double2 *spec, double2 *pspec,
-                         const double2 *twN, const double *sym_s, const double *sym_l,
-                         cudaStream_t s) {
-#define CALL(n) launch_zpass_n<n>(g, mode, spec, pspec, twN, sym_s, sym_l, s)
-  IBK_DISPATCH_N(g.N, CALL)
+                         const double2 *twN, const Sym &sym, cudaStream_t s) {
+#define CALL(n) launch_zpass_n<n>(g, mode, spec, pspec, twN, sym, s)
+  IBK_DISPATCH_N(g.N3, CALL)
 #undef CALL
 }
 
@@ -522,14 +530,14 @@ cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, in
                         const double2 *twN, const double2 *twM, long long *flag,
                         const long long *dev_n, long long n, cudaStream_t s) {
 #define CALL(n_) launch_xinv_n<n_>(g, spec, out, ncomp, twN, twM, flag, dev_n, n, s)
-  IBK_DISPATCH_N(g.N, CALL)
+  IBK_DISPATCH_N(g.N1, CALL)
 #undef CALL
 }
 
-// TMA descriptors of a u-shaped array [3][N][N][N]: RB-row and 1-row boxes of full x rows.
+// TMA descriptors of a u-shaped array [3][N3][N2][N1]: RB-row and 1-row boxes of x rows.
 bool xfwd_encode_u(const FluidGeom &g, const double *u, XMapsU *m) {
   m->ok = false;
-  const int N = g.N;
+  const int N = g.N1;
   if (N > 256 || N < 16) return false;     // box <= 256 doubles; rows >= 128 B (smem alignment)
   void *p = nullptr;
   cudaDriverEntryPointQueryResult q;
@@ -544,7 +552,7 @@ bool xfwd_encode_u(const FluidGeom &g, const double *u, XMapsU *m) {
     case 128: rb = XCfg<128>::RB; break;  case 256: rb = XCfg<256>::RB; break;
     default: return false;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)3 * N * N}, strides[1] = {(cuuint64_t)N * 8};
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)3 * g.N2 * g.N3}, strides[1] = {(cuuint64_t)N * 8};
   cuuint32_t box[2] = {(cuuint32_t)N, (cuuint32_t)rb}, box1[2] = {(cuuint32_t)N, 1u}, es[2] = {1, 1};
   void *base = const_cast<double *>(u);
   if (fn(&m->rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,

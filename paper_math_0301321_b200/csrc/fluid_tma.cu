@@ -68,6 +68,25 @@ template <int N, int MODE> struct ColCfg {
   using K = CT<N, C, G, NC, S>;
 };
 
+// Mixed-radix walk over tiles t = (c * W + w) * NB + x (x fastest) advancing by a fixed
+// stride: one division at the start, carries afterwards (NB, W are runtime values).
+struct Walk {
+  int x, w, c, dx, dw, dc, NB, W;
+  __device__ Walk(int tile, int stride, int NB_, int W_) : NB(NB_), W(W_) {
+    x = tile % NB; w = (tile / NB) % W; c = tile / (NB * W);
+    dx = stride % NB; dw = (stride / NB) % W; dc = stride / (NB * W);
+  }
+  __device__ __forceinline__ void next() {
+    x += dx;
+    int cy = 0;
+    if (x >= NB) { x -= NB; cy = 1; }
+    w += dw + cy;
+    cy = 0;
+    if (w >= W) { w -= W; cy = 1; }
+    c += dc + cy;
+  }
+};
+
 // Tile element (row e, column col) in 16-byte units under the TMA swizzle of the C-wide box.
 template <int C>
 __device__ __forceinline__ int swz(int e, int col) {
@@ -126,18 +145,20 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(ColCfg<N, MODE>::K::NTHR, 1)
 k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
          const __grid_constant__ CUtensorMap map_st, double2 *pspec,
-         const double2 *__restrict__ twN, const double *__restrict__ sym_s,
-         const double *__restrict__ sym_l) {
+         const double2 *__restrict__ twN, Sym sym) {
   using K = typename ColCfg<N, MODE>::K;
   constexpr int C = K::C, G = K::G, T = K::T, NTG = K::NTG, NT = K::NT, S = K::STAGES;
   constexpr int NC = K::NC, BR = K::BOXR;
-  constexpr int M = N / 2, NB = (M + 1 + C - 1) / C;
+  // N = pencil length (N2 for the y modes, N3 for the z modes); W = the other lattice
+  // dimension the tiles walk (z planes for y, ky for z); kx in [0, M], M = N1/2
+  constexpr bool YM = MODE == MODE_YFWD || MODE == MODE_YINV;
+  const int M = g.M, NB = (M + 1 + C - 1) / C, W = YM ? g.N3 : g.N2;
   extern __shared__ __align__(1024) double2 smraw[];
   __shared__ uint64_t full[S], done[S];
   // 1024-byte aligned ring (swizzle atoms); offset arithmetic on the __shared__ array
   // keeps every tile access an LDS/STS (a uintptr_t round trip would make them generic)
   double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
-  const int ntiles = NB * N * (NC == 1 ? 3 : 1);      // NC = 1: (kx block, w, comp) tiles
+  const int ntiles = NB * W * (NC == 1 ? 3 : 1);      // NC = 1: (kx block, w, comp) tiles
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
     fence_mbar_init();
@@ -151,42 +172,46 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
       prefetch_tmap(&map_ld);
       prefetch_tmap(&map_st);
       // tile -> (x offset in doubles, w = ky or z, first component); boxes of BR rows
-      auto load = [&](int tile, int s) {
-        const int x = 2 * C * (tile % NB), w = NC == 1 ? (tile / NB) % N : tile / NB, c0 = NC == 1 ? tile / (NB * N) : 0;
+      auto load = [&](const Walk &t, int s) {
+        const int x = 2 * C * t.x, w = t.w, c0 = NC == 1 ? t.c : 0;
         double2 *b = stage0 + (size_t)s * NC * K::TILE;
         mbar_expect_tx(&full[s], K::STAGE_BYTES);
         for (int c = 0; c < NC; ++c)
           for (int r0 = 0; r0 < N; r0 += BR) {
             double2 *d = b + c * K::TILE + r0 * C;
             if (LD3) tma_load_3d(d, &map_ld, x, w, (c0 + c) * N + r0, &full[s]);
-            else     tma_load_2d(d, &map_ld, x, ((c0 + c) * N + w) * N + r0, &full[s]);
+            else     tma_load_2d(d, &map_ld, x, ((c0 + c) * W + w) * N + r0, &full[s]);
           }
       };
-      auto store = [&](int tile, int s) {
-        const int x = 2 * C * (tile % NB), w = NC == 1 ? (tile / NB) % N : tile / NB, c0 = NC == 1 ? tile / (NB * N) : 0;
+      auto store = [&](const Walk &t, int s) {
+        const int x = 2 * C * t.x, w = t.w, c0 = NC == 1 ? t.c : 0;
         const double2 *b = stage0 + (size_t)s * NC * K::TILE;
         for (int c = 0; c < NC; ++c)
           for (int r0 = 0; r0 < N; r0 += BR) {
             const double2 *d = b + c * K::TILE + r0 * C;
             if (ST3) tma_store_3d(&map_st, x, w, (c0 + c) * N + r0, d);
-            else     tma_store_2d(&map_st, x, ((c0 + c) * N + w) * N + r0, d);
+            else     tma_store_2d(&map_st, x, ((c0 + c) * W + w) * N + r0, d);
           }
         bulk_commit();
       };
+      Walk lw(blockIdx.x, gridDim.x, NB, W), sw(blockIdx.x, gridDim.x, NB, W);
       int i = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
         const int s = i % S;
         if (i >= S) {                                    // slot s held tile i - S
           mbar_wait(&done[s], ((i / S) - 1) & 1);
-          store(tile - S * gridDim.x, s);
+          store(sw, s);
+          sw.next();
           bulk_wait_read0();                             // smem of slot s read out
         }
-        load(tile, s);
+        load(lw, s);
+        lw.next();
       }
       for (int k = i - S < 0 ? 0 : i - S; k < i; ++k) {  // drain the last tiles
         const int s = k % S;
         mbar_wait(&done[s], (k / S) & 1);
-        store(blockIdx.x + k * gridDim.x, s);
+        store(sw, s);
+        sw.next();
       }
       bulk_wait0();
     }
@@ -197,7 +222,9 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG, bar = 1 + grp;
   const int col = gtid % C, t = (gtid / C) % T, comp = gtid / (C * T);
   int i = grp;
-  for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G) {
+  Walk cw(blockIdx.x + grp * gridDim.x, G * gridDim.x, NB, W);
+  const double cdt = g.rho / g.dt, invV = 1.0 / (double)g.V;   // solve constants (MODE_Z)
+  for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G, cw.next()) {
     const int s = i % S;
     mbar_wait(&full[s], (i / S) & 1);
     double2 *buf = stage0 + (size_t)s * NC * K::TILE;
@@ -205,19 +232,22 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
     auto A = [pc, col](int e) -> double2 & { return pc[swz<C>(e, col)]; };
     if (MODE == MODE_Z) {
       fft_inplace<N, -1, C>(A, t, twN, bar, NTG);
-      const int kx0 = C * (tile % NB), ky = tile / NB;   // NC = 3 here
-      const double sy = sym_s[ky], ly = sym_l[ky];
-      const bool ny = (ky == 0) || (ky == M);
-      const double invV = 1.0 / ((double)N * (double)N * (double)N);
-      for (int idx = gtid; idx < N * C; idx += NTG) {
-        const int c = idx % C, kz = idx / C, kx = kx0 + c;
-        if (kx > M) continue;
+      const int kx0 = C * cw.x, ky = cw.w;               // NC = 3 here
+      const double sy = sym.sy[ky], ly = sym.ly[ky];
+      const bool ny = (ky == 0) || (2 * ky == g.N2);
+      // column c = gtid % C is fixed per thread (NTG is a multiple of C): x symbols once
+      static_assert(NTG % C == 0, "solve mapping");
+      const int c = gtid % C, kx = kx0 + c;
+      const bool live = kx <= M;
+      const double sx = live ? sym.sx[kx] : 0.0, lxy = (live ? sym.lx[kx] : 0.0) + ly;
+      const bool nxy = ny && (kx == 0 || kx == M);
+      for (int kz = gtid / C; live && kz < N; kz += NTG / C) {
         double2 *q0 = buf + swz<C>(kz, c);
         double2 *q1 = q0 + K::TILE, *q2 = q1 + K::TILE;
         const double2 r0 = *q0, r1 = *q1, r2 = *q2;
-        const double sx = sym_s[kx], sz = sym_s[kz];
-        const double d = g.rho / g.dt + g.mu * (sym_l[kx] + ly + sym_l[kz]);
-        const bool nul = ny && (kx == 0 || kx == M) && (kz == 0 || kz == M);
+        const double sz = sym.sz[kz];
+        const double d = cdt + g.mu * (lxy + sym.lz[kz]);
+        const bool nul = nxy && (kz == 0 || 2 * kz == N);
         if (nul) {                                       // reading Z6
           const double inv = invV / d;
           *q0 = cscale(r0, inv); *q1 = cscale(r1, inv); *q2 = cscale(r2, inv);
@@ -265,23 +295,25 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 // row pitch P complex); boxes are 2C doubles (C*16 bytes) x N rows with the matching
 // swizzle (C = 8: 128 B, C = 4: 64 B).  Columns past N/2 are zero-filled on load and
 // clipped on store.
-static bool encode(CUtensorMap *m, void *base, int rank, const FluidGeom &g, int C) {
+// rank 2: rows of one spectrum array viewed as [3 * N_outer * L][row], row index
+//         (comp*W + w)*L + e (S1: W = N3, L = N2; S2: W = N2, L = N3 — same row count);
+// rank 3: S2 as (x, z, comp*N2 + ky).  Boxes: 2C doubles x min(L, 256) rows.
+static bool encode(CUtensorMap *m, void *base, int rank, const FluidGeom &g, int C, int L) {
   auto fn = encode_fn();
   if (!fn) return false;
-  const int N = g.N;
   cuuint64_t dims[3], strides[2];
   cuuint32_t box[3], es[3] = {1, 1, 1};
   dims[0] = (cuuint64_t)2 * (g.M + 1);
   strides[0] = (cuuint64_t)g.P * 16;
   box[0] = (cuuint32_t)(2 * C);
-  const cuuint32_t br = (cuuint32_t)(N < 256 ? N : 256);
+  const cuuint32_t br = (cuuint32_t)(L < 256 ? L : 256);
   if (rank == 2) {
-    dims[1] = (cuuint64_t)3 * N * N;
+    dims[1] = (cuuint64_t)3 * g.N2 * g.N3;
     box[1] = br;
   } else {
-    dims[1] = (cuuint64_t)N;                 // z
-    dims[2] = (cuuint64_t)3 * N;             // comp*N + ky
-    strides[1] = (cuuint64_t)N * g.P * 16;
+    dims[1] = (cuuint64_t)g.N3;              // z
+    dims[2] = (cuuint64_t)3 * g.N2;          // comp*N2 + ky
+    strides[1] = (cuuint64_t)g.N3 * g.P * 16;
     box[1] = 1;
     box[2] = br;
   }
@@ -292,21 +324,26 @@ static bool encode(CUtensorMap *m, void *base, int rank, const FluidGeom &g, int
   return r == CUDA_SUCCESS;
 }
 
-static int zcols(int N) { return N >= 128 ? 4 : 8; }   // = ColCfg<N, MODE_Z>::C
+static int zcols(int N3) { return N3 >= 128 ? 4 : 8; }   // = ColCfg<N3, MODE_Z>::C
 
 bool colfft_supported(int N) { return N >= 64 && N <= 512; }
 
 bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m) {
-  return colfft_supported(g.N) && encode(m, base, 2, g, zcols(g.N));
+  return colfft_supported(g.N3) && encode(m, base, 2, g, zcols(g.N3), g.N3);
 }
 
+// y passes need N2 in [64, 512] (maps.y_ok), z passes N3 in [64, 512] (maps.z_ok)
 cudaError_t colfft_make_maps(const FluidGeom &g, double2 *spec, double2 *spec2, TmaMaps *m) {
-  m->ok = false;
-  if (!colfft_supported(g.N)) return cudaSuccess;
-  if (!encode(&m->s1_2d, spec, 2, g, 8) || !encode(&m->s2_3d, spec2, 3, g, 8) ||
-      !encode(&m->s2_2d, spec2, 2, g, zcols(g.N)))
-    return cudaErrorInvalidValue;
-  m->ok = true;
+  m->y_ok = m->z_ok = false;
+  if (colfft_supported(g.N2)) {
+    if (!encode(&m->s1_2d, spec, 2, g, 8, g.N2) || !encode(&m->s2_3d, spec2, 3, g, 8, g.N2))
+      return cudaErrorInvalidValue;
+    m->y_ok = true;
+  }
+  if (colfft_supported(g.N3)) {
+    if (!encode(&m->s2_2d, spec2, 2, g, zcols(g.N3), g.N3)) return cudaErrorInvalidValue;
+    m->z_ok = true;
+  }
   return cudaSuccess;
 }
 
@@ -323,7 +360,7 @@ static int one_per_sm_grid(Kern k, int threads, size_t smem, int ntiles) {
 template <int N, int MODE>
 static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
                                    const CUtensorMap &st, double2 *pspec, const double2 *twN,
-                                   const double *s_, const double *l_, cudaStream_t s) {
+                                   const Sym &sym, cudaStream_t s) {
   using K = typename ColCfg<N, MODE>::K;
   static bool attr = false;
   if (!attr) {
@@ -332,35 +369,36 @@ static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  constexpr int NB = (N / 2 + 1 + K::C - 1) / K::C;   // tiles per w
-  const int grid = one_per_sm_grid(k_colfft<N, MODE>, K::NTHR, K::SMEM, NB * N * (K::NC == 1 ? 3 : 1));
-  k_colfft<N, MODE><<<grid, K::NTHR, K::SMEM, s>>>(g, ld, st, pspec, twN, s_, l_);
+  constexpr bool YM = MODE == MODE_YFWD || MODE == MODE_YINV;
+  const int NB = (g.M + 1 + K::C - 1) / K::C, W = YM ? g.N3 : g.N2;   // tiles per w, w range
+  const int grid = one_per_sm_grid(k_colfft<N, MODE>, K::NTHR, K::SMEM, NB * W * (K::NC == 1 ? 3 : 1));
+  k_colfft<N, MODE><<<grid, K::NTHR, K::SMEM, s>>>(g, ld, st, pspec, twN, sym);
   return cudaGetLastError();
 }
 
 template <int N>
 static cudaError_t colfft_n(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
-                            const double2 *twN, const double *s_, const double *l_,
-                            cudaStream_t s) {
+                            const double2 *twN, const Sym &sym, cudaStream_t s) {
   if constexpr (N >= 64 && N <= 512) {
-    if (mode == MODE_ZINV) return launch_colfft_n<N, MODE_ZINV>(g, m.s2_2d, m.s2_2d, nullptr, twN, s_, l_, s);
-    if (mode == MODE_ZFWD) return launch_colfft_n<N, MODE_ZFWD>(g, m.s2_2d, m.s2_2d, nullptr, twN, s_, l_, s);
-    if (mode == MODE_Z) return launch_colfft_n<N, MODE_Z>(g, m.s2_2d, m.s2_2d, pspec, twN, s_, l_, s);
-    if (mode == MODE_YFWD) return launch_colfft_n<N, MODE_YFWD>(g, m.s1_2d, m.s2_3d, nullptr, twN, s_, l_, s);
-    return launch_colfft_n<N, MODE_YINV>(g, m.s2_3d, m.s1_2d, nullptr, twN, s_, l_, s);
+    if (mode == MODE_ZINV) return launch_colfft_n<N, MODE_ZINV>(g, m.s2_2d, m.s2_2d, nullptr, twN, sym, s);
+    if (mode == MODE_ZFWD) return launch_colfft_n<N, MODE_ZFWD>(g, m.s2_2d, m.s2_2d, nullptr, twN, sym, s);
+    if (mode == MODE_Z) return launch_colfft_n<N, MODE_Z>(g, m.s2_2d, m.s2_2d, pspec, twN, sym, s);
+    if (mode == MODE_YFWD) return launch_colfft_n<N, MODE_YFWD>(g, m.s1_2d, m.s2_3d, nullptr, twN, sym, s);
+    return launch_colfft_n<N, MODE_YINV>(g, m.s2_3d, m.s1_2d, nullptr, twN, sym, s);
   }
   return cudaErrorInvalidValue;
 }
 
+// y modes (1, 2) transform along y (length N2), the z modes (0, 3, 4) along z (N3)
 cudaError_t launch_colfft(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
-                          const double2 *twN, const double *sym_s, const double *sym_l,
-                          cudaStream_t s) {
-  if (!m.ok) return cudaErrorInvalidValue;
-  switch (g.N) {
-    case 64: return colfft_n<64>(g, mode, m, pspec, twN, sym_s, sym_l, s);
-    case 128: return colfft_n<128>(g, mode, m, pspec, twN, sym_s, sym_l, s);
-    case 256: return colfft_n<256>(g, mode, m, pspec, twN, sym_s, sym_l, s);
-    case 512: return colfft_n<512>(g, mode, m, pspec, twN, sym_s, sym_l, s);
+                          const double2 *twN, const Sym &sym, cudaStream_t s) {
+  const bool ym = mode == MODE_YFWD || mode == MODE_YINV;
+  if (ym ? !m.y_ok : !m.z_ok) return cudaErrorInvalidValue;
+  switch (ym ? g.N2 : g.N3) {
+    case 64: return colfft_n<64>(g, mode, m, pspec, twN, sym, s);
+    case 128: return colfft_n<128>(g, mode, m, pspec, twN, sym, s);
+    case 256: return colfft_n<256>(g, mode, m, pspec, twN, sym, s);
+    case 512: return colfft_n<512>(g, mode, m, pspec, twN, sym, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -98,46 +98,49 @@ void free_graph(ib_ctx *c) {
   c->graph_key = -1;
 }
 
-// The three strided spectrum passes: TMA column kernels when available (N in [64, 256]),
-// else the cp.async pencil kernels.
-cudaError_t yfwd(ib_ctx *c, cudaStream_t s) {
-  if (c->maps.ok) return launch_colfft(c->g, 1, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s);
-  return launch_ypass(c->g, -1, c->spec, 1, c->spec2, 2, 3, c->twN, s);
-}
-cudaError_t zsolve(ib_ctx *c, double2 *pspec, cudaStream_t s) {
-  if (c->maps.ok) return launch_colfft(c->g, 0, c->maps, pspec, c->twN, c->sym_s, c->sym_l, s);
-  return launch_zpass(c->g, 0, c->spec2, pspec, c->twN, c->sym_s, c->sym_l, s);
-}
-cudaError_t yinv(ib_ctx *c, cudaStream_t s) {
-  if (c->maps.ok) return launch_colfft(c->g, 2, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s);
-  return launch_ypass(c->g, +1, c->spec2, 2, c->spec, 1, 3, c->twN, s);
+Sym sym_of(const ib_ctx *c) {
+  return Sym{c->sym_s[0], c->sym_l[0], c->sym_s[1], c->sym_l[1], c->sym_s[2], c->sym_l[2]};
 }
 
-// Pressure half-spectrum p^ written by the z solve (S2 layout) -> p [N^3] real.  With the
-// TMA passes p^ is in full (ky, kz, kx) order and ps must hold 3 component slots (the
+// The three strided spectrum passes: TMA column kernels when available (pencil length in
+// [64, 512]), else the cp.async pencil kernels.
+cudaError_t yfwd(ib_ctx *c, cudaStream_t s) {
+  if (c->maps.y_ok) return launch_colfft(c->g, 1, c->maps, nullptr, c->tw[1], sym_of(c), s);
+  return launch_ypass(c->g, -1, c->spec, 1, c->spec2, 2, 3, c->tw[1], s);
+}
+cudaError_t zsolve(ib_ctx *c, double2 *pspec, cudaStream_t s) {
+  if (c->maps.z_ok) return launch_colfft(c->g, 0, c->maps, pspec, c->tw[2], sym_of(c), s);
+  return launch_zpass(c->g, 0, c->spec2, pspec, c->tw[2], sym_of(c), s);
+}
+cudaError_t yinv(ib_ctx *c, cudaStream_t s) {
+  if (c->maps.y_ok) return launch_colfft(c->g, 2, c->maps, nullptr, c->tw[1], sym_of(c), s);
+  return launch_ypass(c->g, +1, c->spec2, 2, c->spec, 1, 3, c->tw[1], s);
+}
+
+// Pressure half-spectrum p^ written by the z solve (S2 layout) -> p [V] real.  With the
+// TMA z pass p^ is in full (ky, kz, kx) order and ps must hold 3 component slots (the
 // inverse-z column pass transforms all three; slots 1-2 are scratch).
 cudaError_t pressure_to_real(ib_ctx *c, double2 *ps, double2 *ps1, double *out, cudaStream_t s) {
   cudaError_t e;
-  if (c->maps.ok) {
+  if (c->maps.z_ok) {
     TmaMaps m;
     if (!colfft_encode_s2(c->g, ps, &m.s2_2d)) return cudaErrorInvalidValue;
-    m.ok = true;
-    if ((e = launch_colfft(c->g, 4, m, nullptr, c->twN, c->sym_s, c->sym_l, s)) != cudaSuccess) return e;
+    m.z_ok = true;
+    if ((e = launch_colfft(c->g, 4, m, nullptr, c->tw[2], sym_of(c), s)) != cudaSuccess) return e;
   }
-  if ((e = launch_ypass(c->g, +1, ps, 2, ps1, 1, 1, c->twN, s)) != cudaSuccess) return e;
-  return launch_xinv(c->g, ps1, out, 1, c->twN, c->twM, nullptr, nullptr, 0, s);
+  if ((e = launch_ypass(c->g, +1, ps, 2, ps1, 1, 1, c->tw[1], s)) != cudaSuccess) return e;
+  return launch_xinv(c->g, ps1, out, 1, c->tw[0], c->twM, nullptr, nullptr, 0, s);
 }
 
-size_t pspec_elems(const ib_ctx *c) {
-  return (size_t)(c->maps.ok ? 3 : 1) * c->g.N * c->g.N * c->g.P;
-}
+size_t spec1_elems(const ib_ctx *c) { return (size_t)c->g.N2 * c->g.N3 * c->g.P; }
+size_t pspec_elems(const ib_ctx *c) { return (size_t)(c->maps.z_ok ? 3 : 1) * spec1_elems(c); }
 
 // x passes: the forward pass is fluid.cu's k_xfwd; the inverse uses the TMA kernel when
 // available (N in [64, 256]).
 cudaError_t xfwd(ib_ctx *c, int mode, const double *u, double *F, unsigned *rowflag,
                  double *r_out, cudaStream_t s) {
   if (mode == 2)
-    return launch_xfwd(c->g, 2, nullptr, nullptr, nullptr, u, nullptr, c->spec, c->twN, c->twM,
+    return launch_xfwd(c->g, 2, nullptr, nullptr, nullptr, u, nullptr, c->spec, c->tw[0], c->twM,
                        nullptr, s);
   XMapsU tmp;
   const XMapsU *um = &c->umaps;
@@ -145,12 +148,12 @@ cudaError_t xfwd(ib_ctx *c, int mode, const double *u, double *F, unsigned *rowf
     xfwd_encode_u(c->g, u, &tmp);
     um = &tmp;
   }
-  return launch_xfwd(c->g, mode, u, F, rowflag, nullptr, r_out, c->spec, c->twN, c->twM, um, s);
+  return launch_xfwd(c->g, mode, u, F, rowflag, nullptr, r_out, c->spec, c->tw[0], c->twM, um, s);
 }
 cudaError_t xinv(ib_ctx *c, double *out, const long long *dev_n, long long n, long long *flag,
                  cudaStream_t s) {
-  if (c->xok) return launch_xinv_tma(c->g, c->smaps, out, c->twN, c->twM, flag, dev_n, n, s);
-  return launch_xinv(c->g, c->spec, out, 3, c->twN, c->twM, flag, dev_n, n, s);
+  if (c->xok) return launch_xinv_tma(c->g, c->smaps, out, c->tw[0], c->twM, flag, dev_n, n, s);
+  return launch_xinv(c->g, c->spec, out, 3, c->tw[0], c->twM, flag, dev_n, n, s);
 }
 
 // (Re)bin the points by base cell when the permutation is missing or SORT_PERIOD steps old.
@@ -229,15 +232,34 @@ extern "C" {
 
 const char *ib_last_error(void) { return g_err.c_str(); }
 
-ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
-  if (N < 8 || N > 512 || (N & (N - 1))) { fail(IB_EINVAL, "N must be a power of two in [8, 512]"); return nullptr; }
+static bool pow2_in(int32_t n, int32_t lo, int32_t hi) { return n >= lo && n <= hi && !(n & (n - 1)); }
+
+// rows per x-pass tile for a row length N1 (= XCfg<N1>::RB): the y extent N2 must be a
+// multiple of it
+static int32_t x_rows(int32_t N1) {
+  const int32_t M = N1 / 2, T = M >= 16 ? M / 16 : 1, rb = 64 / T;
+  return rb < N1 ? rb : N1;
+}
+
+ib_ctx *ib_create3(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu,
+                   double dt) {
+  if (!pow2_in(N1, 8, 512) || !pow2_in(N2, 8, 512) || !pow2_in(N3, 8, 512)) {
+    fail(IB_EINVAL, "N1, N2, N3 must be powers of two in [8, 512]");
+    return nullptr;
+  }
+  if (N2 % x_rows(N1)) {
+    fail(IB_EINVAL, "N2 must be a multiple of " + std::to_string(x_rows(N1)) + " for N1 = " +
+                        std::to_string(N1));
+    return nullptr;
+  }
   if (!(h > 0) || !std::isfinite(h)) { fail(IB_EINVAL, "h must be > 0"); return nullptr; }
   if (!(rho > 0) || !std::isfinite(rho)) { fail(IB_EINVAL, "rho must be > 0"); return nullptr; }
   if (!(mu >= 0) || !std::isfinite(mu)) { fail(IB_EINVAL, "mu must be >= 0"); return nullptr; }
   if (!(dt > 0) || !std::isfinite(dt)) { fail(IB_EINVAL, "dt must be > 0"); return nullptr; }
   ib_ctx *c = new ib_ctx();
-  c->g.N = N; c->g.M = N / 2; c->g.P = N / 2 + 2;
-  c->g.V = (int64_t)N * N * N;
+  c->g.N1 = N1; c->g.N2 = N2; c->g.N3 = N3;
+  c->g.M = N1 / 2; c->g.P = N1 / 2 + 2;
+  c->g.V = (int64_t)N1 * N2 * N3;
   c->g.h = h; c->g.invh = 1.0 / h; c->g.rho = rho; c->g.mu = mu; c->g.dt = dt;
   auto bad = [&](cudaError_t e, const char *what) {
     fail(e == cudaErrorMemoryAllocation ? IB_ENOMEM : IB_ECUDA,
@@ -249,17 +271,20 @@ ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
   if ((e = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking)) != cudaSuccess) return bad(e, "stream");
   c->stream = c->own_stream;
   const size_t V = (size_t)c->g.V;
-  const size_t S = (size_t)3 * N * N * c->g.P;
+  const size_t S = (size_t)3 * spec1_elems(c);
   if ((e = dalloc(&c->u, 3 * V)) != cudaSuccess) return bad(e, "u");
   if ((e = dalloc(&c->F, 3 * V)) != cudaSuccess) return bad(e, "F");
   if ((e = dalloc(&c->spec, S)) != cudaSuccess) return bad(e, "spectrum");
   if ((e = dalloc(&c->spec2, S)) != cudaSuccess) return bad(e, "spectrum");
-  if ((e = dalloc(&c->rowflag, (size_t)N * N)) != cudaSuccess) return bad(e, "row flags");
-  if ((e = cudaMemsetAsync(c->rowflag, 0, (size_t)N * N * sizeof(unsigned), c->stream)) != cudaSuccess) return bad(e, "memset");
-  if ((e = dalloc(&c->twN, N)) != cudaSuccess) return bad(e, "tables");
-  if ((e = dalloc(&c->twM, N / 2)) != cudaSuccess) return bad(e, "tables");
-  if ((e = dalloc(&c->sym_s, N)) != cudaSuccess) return bad(e, "tables");
-  if ((e = dalloc(&c->sym_l, N)) != cudaSuccess) return bad(e, "tables");
+  if ((e = dalloc(&c->rowflag, (size_t)N2 * N3)) != cudaSuccess) return bad(e, "row flags");
+  if ((e = cudaMemsetAsync(c->rowflag, 0, (size_t)N2 * N3 * sizeof(unsigned), c->stream)) != cudaSuccess) return bad(e, "memset");
+  const int32_t L[3] = {N1, N2, N3};
+  for (int a = 0; a < 3; ++a) {
+    if ((e = dalloc(&c->tw[a], (size_t)L[a])) != cudaSuccess) return bad(e, "tables");
+    if ((e = dalloc(&c->sym_s[a], (size_t)L[a])) != cudaSuccess) return bad(e, "tables");
+    if ((e = dalloc(&c->sym_l[a], (size_t)L[a])) != cudaSuccess) return bad(e, "tables");
+  }
+  if ((e = dalloc(&c->twM, N1 / 2)) != cudaSuccess) return bad(e, "tables");
   if ((e = dalloc(&c->flag, 1)) != cudaSuccess) return bad(e, "flag");
   if ((e = dalloc(&c->dev_n, 1)) != cudaSuccess) return bad(e, "flag");
   if ((e = cudaMallocHost(&c->flag_h, sizeof(long long))) != cudaSuccess) return bad(e, "flag");
@@ -267,13 +292,14 @@ ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
     if ((e = cudaEventCreate(&c->ev[k])) != cudaSuccess) return bad(e, "events");
   if ((e = cudaMemsetAsync(c->u, 0, 3 * V * sizeof(double), c->stream)) != cudaSuccess) return bad(e, "memset");
   if ((e = cudaMemsetAsync(c->F, 0, 3 * V * sizeof(double), c->stream)) != cudaSuccess) return bad(e, "memset");
-  if ((e = fluid_setup_attributes(N)) != cudaSuccess) return bad(e, "attributes");
+  for (int a = 0; a < 3; ++a)
+    if ((e = fluid_setup_attributes(L[a])) != cudaSuccess) return bad(e, "attributes");
   if ((e = colfft_make_maps(c->g, c->spec, c->spec2, &c->maps)) != cudaSuccess) return bad(e, "TMA tensor maps");
 #ifndef IBK_NO_XFTMA
-  xfwd_encode_u(c->g, c->u, &c->umaps);   // !ok (cp.async tile copy) when N > 256
+  xfwd_encode_u(c->g, c->u, &c->umaps);   // !ok (cp.async tile copy) when N1 > 256
 #endif
 #ifndef IBK_NO_XTMA   // dev switch: the per-CTA row kernels of fluid.cu for comparison
-  if (xpass_supported(N)) {
+  if (xpass_supported(N1)) {
     if (!xpass_encode_s1(c->g, c->spec, &c->smaps))
       return bad(cudaErrorInvalidValue, "TMA tensor maps (x passes)");
     c->xok = true;
@@ -284,12 +310,17 @@ ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
   return c;
 }
 
+ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt) {
+  return ib_create3(N, N, N, h, rho, mu, dt);
+}
+
 void ib_destroy(ib_ctx *c) {
   if (!c) return;
   if (c->stream) cudaStreamSynchronize(c->stream);
   free_graph(c);
   dfree(c->u); dfree(c->F); dfree(c->rowflag); dfree(c->spec); dfree(c->spec2); dfree(c->pspec); dfree(c->pspec1); dfree(c->p);
-  dfree(c->twN); dfree(c->twM); dfree(c->sym_s); dfree(c->sym_l);
+  for (int a = 0; a < 3; ++a) { dfree(c->tw[a]); dfree(c->sym_s[a]); dfree(c->sym_l[a]); }
+  dfree(c->twM);
   dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->drive_idx); dfree(c->drive_dir);
   dfree(c->perm); dfree(c->bincnt); dfree(c->binsum);
   dfree(c->flag); dfree(c->dev_n);
@@ -315,7 +346,7 @@ int ib_set_option(ib_ctx *c, int32_t opt, int64_t value) {
       c->want_p = value != 0;
       if (c->want_p && !c->pspec) {
         CK(dalloc(&c->pspec, pspec_elems(c)));
-        CK(dalloc(&c->pspec1, (size_t)c->g.N * c->g.N * c->g.P));
+        CK(dalloc(&c->pspec1, spec1_elems(c)));
         CK(dalloc(&c->p, (size_t)c->g.V));
       }
       return IB_OK;
@@ -519,7 +550,7 @@ int ib_get_fields(ib_ctx *c, double *u, double *p) {
   if (p) {
     if (!c->have_p || !c->pspec) return fail(IB_ESTATE, "pressure not available: enable IB_OPT_PRESSURE before ib_step");
     CK(pressure_to_real(c, c->pspec, c->pspec1, c->p, c->stream));
-    c->launches += c->maps.ok ? 3 : 2;
+    c->launches += c->maps.z_ok ? 3 : 2;
     CK(copy_sync(p, c->p, (size_t)c->g.V * sizeof(double), c->stream));
   }
   return IB_OK;
@@ -631,7 +662,7 @@ int ib_debug_fluid(ib_ctx *c, const double *u, const double *F, double *u_out, d
   cudaStream_t s = c->stream;
   CK(t.get(&ud, 3 * V)); CK(t.get(&Fd, 3 * V));
   if (p_out) {
-    CK(t.get(&ps, pspec_elems(c))); CK(t.get(&ps1, (size_t)g.N * g.N * g.P));
+    CK(t.get(&ps, pspec_elems(c))); CK(t.get(&ps1, spec1_elems(c)));
     CK(t.get(&pd, V));
   }
   CK(copy_sync(ud, u, 3 * V * sizeof(double), s));
@@ -658,18 +689,16 @@ int ib_debug_fft(ib_ctx *c, const double *in, double *out) {
   CK(t.get(&ind, V));
   CK(copy_sync(ind, in, V * sizeof(double), s));
   CK(xfwd(c, 2, ind, nullptr, nullptr, nullptr, s));
-  if (c->maps.ok) {      // TMA passes transform all 3 component slots (only slot 0 is read)
-    CK(launch_colfft(g, 1, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s));
-    CK(launch_colfft(g, 3, c->maps, nullptr, c->twN, c->sym_s, c->sym_l, s));
-  } else {
-    CK(launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 1, c->twN, s));
-    CK(launch_zpass(g, 1, c->spec2, nullptr, c->twN, c->sym_s, c->sym_l, s));
-  }
+  // (TMA passes transform all 3 component slots; only slot 0 is read)
+  if (c->maps.y_ok) CK(launch_colfft(g, 1, c->maps, nullptr, c->tw[1], sym_of(c), s));
+  else CK(launch_ypass(g, -1, c->spec, 1, c->spec2, 2, 1, c->tw[1], s));
+  if (c->maps.z_ok) CK(launch_colfft(g, 3, c->maps, nullptr, c->tw[2], sym_of(c), s));
+  else CK(launch_zpass(g, 1, c->spec2, nullptr, c->tw[2], sym_of(c), s));
   // S2 [ky][kz][kx] -> out [kz][ky][kx]
-  for (int ky = 0; ky < g.N; ++ky)
-    CK(cudaMemcpy2DAsync(out + (size_t)ky * (g.M + 1) * 2, (size_t)g.N * (g.M + 1) * 2 * sizeof(double),
-                         c->spec2 + (size_t)ky * g.N * g.P, (size_t)g.P * sizeof(double2),
-                         (size_t)(g.M + 1) * sizeof(double2), (size_t)g.N, cudaMemcpyDefault, s));
+  for (int ky = 0; ky < g.N2; ++ky)
+    CK(cudaMemcpy2DAsync(out + (size_t)ky * (g.M + 1) * 2, (size_t)g.N2 * (g.M + 1) * 2 * sizeof(double),
+                         c->spec2 + (size_t)ky * g.N3 * g.P, (size_t)g.P * sizeof(double2),
+                         (size_t)(g.M + 1) * sizeof(double2), (size_t)g.N3, cudaMemcpyDefault, s));
   CK(cudaStreamSynchronize(s));
   return IB_OK;
 }

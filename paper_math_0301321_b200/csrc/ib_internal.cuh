@@ -26,17 +26,25 @@ struct StructDev {
   int32_t drive_period;
 };
 
-// Per-N launch configuration of the fluid passes.
+// Lattice of the fluid passes: N1 x N2 x N3 points along x, y, z (powers of two), mesh width
+// h in every direction (the paper's lattice of width h, PAPER.md 632-633; anisotropic boxes
+// such as its 256 x 256 x 128 half-cube, 1003-1007).
 struct FluidGeom {
-  int N, M, P;                // M = N/2; P = spectrum row pitch in complex (>= M+1)
-  int64_t V;
+  int N1, N2, N3;
+  int M, P;                   // M = N1/2; P = spectrum row pitch in complex (>= M+1)
+  int64_t V;                  // N1 N2 N3
   double h, invh, rho, mu, dt;
+};
+
+// Per-axis symbols (D0 symbol s, -symbol of D+D- l) of the three lattice axes.
+struct Sym {
+  const double *sx, *lx, *sy, *ly, *sz, *lz;
 };
 
 // TMA descriptors of the two spectrum arrays (fluid_tma.cu), valid when ok.
 struct TmaMaps {
   CUtensorMap s1_2d, s2_2d, s2_3d;
-  bool ok = false;
+  bool y_ok = false, z_ok = false;   // y passes (s1_2d, s2_3d) / z passes (s2_2d) available
 };
 
 // TMA descriptors of the forward x pass (fluid.cu): u rows, RB-row and 1-row boxes.
@@ -68,8 +76,9 @@ struct ib_ctx {
   double2 *pspec = nullptr;     // pressure, S2 layout (lazily)
   double2 *pspec1 = nullptr;    // pressure, S1 layout (lazily)
   double *p = nullptr;          // [V] pressure output cache (lazily)
-  double2 *twN = nullptr, *twM = nullptr;   // exp(-2 pi i t/L) tables
-  double *sym_s = nullptr, *sym_l = nullptr; // per-axis symbols
+  double2 *tw[3] = {};                       // exp(-2 pi i t/N_a), per axis a = x, y, z
+  double2 *twM = nullptr;                    // exp(-2 pi i t/(N1/2))
+  double *sym_s[3] = {}, *sym_l[3] = {};     // per-axis symbols
   ibk::TmaMaps maps;                         // TMA column-pass descriptors (N in [64, 256])
   ibk::XMapsS smaps;                         // TMA x-inverse descriptors of spec
   ibk::XMapsU umaps;                         // TMA x-forward descriptors of u (N <= 256)
@@ -124,8 +133,7 @@ cudaError_t launch_ypass(const FluidGeom &g, int sign, const double2 *in, int in
 // z pass on an S2 spectrum: mode 0 = fwd+project+inv (pressure if pspec != null, S2),
 // 1 = forward only
 cudaError_t launch_zpass(const FluidGeom &g, int mode, double2 *spec, double2 *pspec,
-                         const double2 *twN, const double *sym_s, const double *sym_l,
-                         cudaStream_t s);
+                         const double2 *twN, const Sym &sym, cudaStream_t s);
 cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, int ncomp,
                         const double2 *twN, const double2 *twM, long long *flag,
                         const long long *dev_n, long long n, cudaStream_t s);
@@ -135,9 +143,9 @@ cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, in
 bool colfft_supported(int N);
 bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m);
 cudaError_t colfft_make_maps(const FluidGeom &g, double2 *spec, double2 *spec2, TmaMaps *m);
+// twN: twiddles of the pencil axis (y for modes 1-2, z for 0, 3, 4)
 cudaError_t launch_colfft(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
-                          const double2 *twN, const double *sym_s, const double *sym_l,
-                          cudaStream_t s);
+                          const double2 *twN, const Sym &sym, cudaStream_t s);
 // TMA inverse x pass (xpass_tma.cu), N in [64, 256]: S1 -> out (3 components)
 bool xpass_supported(int N);
 bool xpass_encode_s1(const FluidGeom &g, const double2 *spec, XMapsS *m);

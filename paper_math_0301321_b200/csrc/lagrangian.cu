@@ -132,7 +132,7 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
   const int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (d >= sd.nd) return;
-  const int N = g.N;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const size_t V = (size_t)g.V;
   const double a = drive_factor(sd, dev_n ? *dev_n : n) * g.invh * g.invh * g.invh;
   if (a == 0.0) return;
@@ -142,14 +142,14 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
   const int jy = axis_weights(sd.X[3 * i + 1], g.invh, wy);
   const int jz = axis_weights(sd.X[3 * i + 2], g.invh, wz);
   const int e = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
-  const size_t x = (jx + e) & (N - 1), y = (jy + b) & (N - 1);
+  const size_t x = (jx + e) & (N1 - 1), y = (jy + b) & (N2 - 1);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const size_t z = (jz + c0 + 2 * h) & (N - 1);
-    const size_t cell = (z * N + y) * N + x;
+    const size_t z = (jz + c0 + 2 * h) & (N3 - 1);
+    const size_t cell = (z * N2 + y) * N1 + x;
     const double w = a * wx[e] * wy[b] * wz[c0 + 2 * h];
     for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], w * sd.drive_dir[3 * d + k]);
-    if (rowflag && e == 0) rowflag[z * N + y] = 1u;
+    if (rowflag && e == 0) rowflag[z * N2 + y] = 1u;
   }
 }
 
@@ -172,7 +172,7 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
   __syncthreads();
   const ib_patch *pt = small ? ptab : sd.patches;
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int N = g.N;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const size_t V = (size_t)g.V;
   double *r = rec[warp][lane];
   unsigned key = 0xffffffffu;
@@ -195,14 +195,14 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
     }
     const double ih3 = g.invh * g.invh * g.invh;
     live = (f[0] != 0.0) || (f[1] != 0.0) || (f[2] != 0.0);
-    const int jx = axis_weights(__ldg(&sd.X[3 * i + 0]), g.invh, r + 0) & (N - 1);
-    const int jy = axis_weights(__ldg(&sd.X[3 * i + 1]), g.invh, r + 4) & (N - 1);
-    const int jz = axis_weights(__ldg(&sd.X[3 * i + 2]), g.invh, r + 8) & (N - 1);
+    const int jx = axis_weights(__ldg(&sd.X[3 * i + 0]), g.invh, r + 0) & (N1 - 1);
+    const int jy = axis_weights(__ldg(&sd.X[3 * i + 1]), g.invh, r + 4) & (N2 - 1);
+    const int jz = axis_weights(__ldg(&sd.X[3 * i + 2]), g.invh, r + 8) & (N3 - 1);
     r[12] = f[0] * ih3; r[13] = f[1] * ih3; r[14] = f[2] * ih3;
-    key = ((unsigned)jz * N + (unsigned)jy) * N + (unsigned)jx;
+    key = ((unsigned)jz * N2 + (unsigned)jy) * N1 + (unsigned)jx;
   }
   __syncwarp();
-  const int lgN = __ffs(N) - 1;          // N is a power of two: no integer division below
+  const int lg1 = __ffs(N1) - 1, lg2 = __ffs(N2) - 1;   // powers of two: no division below
   unsigned todo = __ballot_sync(0xffffffffu, live);
 #ifdef IBK_SP_NOGROUPS   // dev timing experiment only
   if (live && r[12] == 1.2345e300) F[0] = 1.0;
@@ -233,10 +233,10 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
       acc[2] += q[13] * w0 + q2[13] * v0; acc[3] += q[13] * w1 + q2[13] * v1;
       acc[4] += q[14] * w0 + q2[14] * v0; acc[5] += q[14] * w1 + q2[14] * v1;
     }
-    const unsigned jx = kl & (N - 1), jy = (kl >> lgN) & (N - 1), jz = kl >> (2 * lgN);
-    const size_t x = (jx + a) & (N - 1), y = (jy + b) & (N - 1);
-    const size_t z0 = (jz + c0) & (N - 1), z1 = (jz + c0 + 2) & (N - 1);
-    const size_t e0 = (z0 * N + y) * N + x, e1 = (z1 * N + y) * N + x;
+    const unsigned jx = kl & (N1 - 1), jy = (kl >> lg1) & (N2 - 1), jz = kl >> (lg1 + lg2);
+    const size_t x = (jx + a) & (N1 - 1), y = (jy + b) & (N2 - 1);
+    const size_t z0 = (jz + c0) & (N3 - 1), z1 = (jz + c0 + 2) & (N3 - 1);
+    const size_t e0 = (z0 * N2 + y) * N1 + x, e1 = (z1 * N2 + y) * N1 + x;
 #ifdef IBK_SP_NOFLUSH   // dev timing experiment only
     if (acc[0] == 1.2345e300)
 #endif
@@ -244,8 +244,8 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
     atomicAdd(&F[V + e0], acc[2]);      atomicAdd(&F[V + e1], acc[3]);
     atomicAdd(&F[2 * V + e0], acc[4]);  atomicAdd(&F[2 * V + e1], acc[5]);
     if (rowflag && a == 0) {                    // mark rows (y, z0), (y, z1) of F non-zero
-      rowflag[z0 * N + y] = 1u;
-      rowflag[z1 * N + y] = 1u;
+      rowflag[z0 * N2 + y] = 1u;
+      rowflag[z1 * N2 + y] = 1u;
     }
   }
 }
@@ -276,7 +276,8 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
 // U = sum_c wz_c sum_b wy_b (sum_a wx_a u(jx+a, jy+b, jz+c)) straight from global memory
 // (row sums first, 32-bit cell offsets; a row with no periodic wrap in x is 4 consecutive
 // doubles off one base pointer).  Used by warps whose points span more than BOXES boxes.
-__device__ __forceinline__ void interp_direct(const double *__restrict__ u, int N, int Vi,
+__device__ __forceinline__ void interp_direct(const double *__restrict__ u, int N1, int N2,
+                                              int N3, int Vi,
                                               int jx, int jy, int jz, const double wx[4],
                                               const double wy[4], const double wz[4],
                                               double &U0, double &U1, double &U2) {
@@ -285,9 +286,9 @@ __device__ __forceinline__ void interp_direct(const double *__restrict__ u, int 
   for (int c = 0; c < 4; ++c)
 #pragma unroll
     for (int b = 0; b < 4; ++b)
-      ro[c][b] = (((jz + c) & (N - 1)) * N + ((jy + b) & (N - 1))) * N;
+      ro[c][b] = (((jz + c) & (N3 - 1)) * N2 + ((jy + b) & (N2 - 1))) * N1;
   U0 = U1 = U2 = 0.0;
-  if (jx >= 0 && jx + 3 < N) {
+  if (jx >= 0 && jx + 3 < N1) {
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -302,7 +303,7 @@ __device__ __forceinline__ void interp_direct(const double *__restrict__ u, int 
   } else {
     int xo[4];
 #pragma unroll
-    for (int a = 0; a < 4; ++a) xo[a] = (jx + a) & (N - 1);
+    for (int a = 0; a < 4; ++a) xo[a] = (jx + a) & (N1 - 1);
 #pragma unroll
     for (int c = 0; c < 4; ++c)
 #pragma unroll
@@ -335,7 +336,7 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
   __shared__ double box[INTERP_THREADS / 32][BOXES][BOXLD];
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int N = g.N;
+  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const int Vi = (int)g.V;
   const bool live = k < np;
   bool bad = false;
@@ -346,7 +347,7 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
   const int jx = axis_weights(x0, g.invh, wx);
   const int jy = axis_weights(x1, g.invh, wy);
   const int jz = axis_weights(x2, g.invh, wz);
-  const unsigned key = ((unsigned)(jz & (N - 1)) * N + (unsigned)(jy & (N - 1))) * N + (unsigned)(jx & (N - 1));
+  const unsigned key = ((unsigned)(jz & (N3 - 1)) * N2 + (unsigned)(jy & (N2 - 1))) * N1 + (unsigned)(jx & (N1 - 1));
   const unsigned active = __ballot_sync(0xffffffffu, live);
   const unsigned peers = __match_any_sync(0xffffffffu, live ? key : 0xffffffffu) & active;
   const unsigned leaders = __ballot_sync(0xffffffffu, live && lane == __ffs(peers) - 1);
@@ -359,12 +360,12 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
       lm &= lm - 1;
       const int gx = __shfl_sync(0xffffffffu, jx, ld), gy = __shfl_sync(0xffffffffu, jy, ld),
                 gz = __shfl_sync(0xffffffffu, jz, ld);
-      const int xo = (gx + a) & (N - 1), yo = (gy + b) & (N - 1);
+      const int xo = (gx + a) & (N1 - 1), yo = (gy + b) & (N2 - 1);
       double *bx = box[warp][gi];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = c0 + 2 * h;
-        const int cell = (((gz + c) & (N - 1)) * N + yo) * N + xo;
+        const int cell = (((gz + c) & (N3 - 1)) * N2 + yo) * N1 + xo;
         const int node = (c * 4 + b) * 4 + a;
         bx[node] = __ldg(u + cell);
         bx[64 + node] = __ldg(u + Vi + cell);
@@ -387,7 +388,7 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
         U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
       }
   } else {
-    interp_direct(u, N, Vi, jx, jy, jz, wx, wy, wz, U0, U1, U2);
+    interp_direct(u, N1, N2, N3, Vi, jx, jy, jz, wx, wy, wz, U0, U1, U2);
   }
   if (live) {
     if (U_out) {
@@ -427,18 +428,19 @@ cudaError_t launch_step_inc(long long *dev_n, cudaStream_t s) {
 // (a counting sort over the N^3 cells: count, exclusive scan, scatter).  Only the order in
 // which spread/interp visit points depends on it, never a result beyond fp64 summation
 // order; ib_step refreshes it every IB_SORT_PERIOD steps.
-__device__ __forceinline__ unsigned cell_key(const double *X, int64_t i, double invh, int N) {
-  const int cx = (int)(long long)floor(X[3 * i + 0] * invh) & (N - 1);
-  const int cy = (int)(long long)floor(X[3 * i + 1] * invh) & (N - 1);
-  const int cz = (int)(long long)floor(X[3 * i + 2] * invh) & (N - 1);
-  return ((unsigned)cz * N + (unsigned)cy) * N + (unsigned)cx;
+__device__ __forceinline__ unsigned cell_key(const double *X, int64_t i, double invh, int N1,
+                                             int N2, int N3) {
+  const int cx = (int)(long long)floor(X[3 * i + 0] * invh) & (N1 - 1);
+  const int cy = (int)(long long)floor(X[3 * i + 1] * invh) & (N2 - 1);
+  const int cz = (int)(long long)floor(X[3 * i + 2] * invh) & (N3 - 1);
+  return ((unsigned)cz * N2 + (unsigned)cy) * N1 + (unsigned)cx;
 }
 
-__global__ void k_bin_count(const double *__restrict__ X, int64_t np, double invh, int N,
-                            unsigned *cnt) {
+__global__ void k_bin_count(const double *__restrict__ X, int64_t np, double invh, int N1,
+                            int N2, int N3, unsigned *cnt) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool ok = i < np;
-  const unsigned key = ok ? cell_key(X, i, invh, N) : 0xffffffffu;
+  const unsigned key = ok ? cell_key(X, i, invh, N1, N2, N3) : 0xffffffffu;
   const unsigned peers = __match_any_sync(0xffffffffu, key);
   if (ok && (threadIdx.x & 31) == (unsigned)(__ffs(peers) - 1)) atomicAdd(&cnt[key], __popc(peers));
 }
@@ -507,11 +509,11 @@ __global__ void __launch_bounds__(SCAN_T) k_scan_final(unsigned *cnt, size_t n, 
     if (base + e < n) { cnt[base + e] = run; run += v[e]; }
 }
 
-__global__ void k_bin_scatter(const double *__restrict__ X, int64_t np, double invh, int N,
-                              unsigned *off, int *perm) {
+__global__ void k_bin_scatter(const double *__restrict__ X, int64_t np, double invh, int N1,
+                              int N2, int N3, unsigned *off, int *perm) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool ok = i < np;
-  const unsigned key = ok ? cell_key(X, i, invh, N) : 0xffffffffu;
+  const unsigned key = ok ? cell_key(X, i, invh, N1, N2, N3) : 0xffffffffu;
   const unsigned peers = __match_any_sync(0xffffffffu, key);
   const int lane = threadIdx.x & 31, leader = __ffs(peers) - 1;
   unsigned base = 0;
@@ -528,11 +530,11 @@ cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned
   const unsigned pb = (unsigned)((np + 255) / 256);
   cudaError_t e = cudaMemsetAsync(cnt, 0, n * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
-  k_bin_count<<<pb, 256, 0, s>>>(X, np, g.invh, g.N, cnt);
+  k_bin_count<<<pb, 256, 0, s>>>(X, np, g.invh, g.N1, g.N2, g.N3, cnt);
   k_scan_partial<<<nb, SCAN_T, 0, s>>>(cnt, n, bsum);
   k_scan_bsum<<<1, SCAN_T, 0, s>>>(bsum, nb);
   k_scan_final<<<nb, SCAN_T, 0, s>>>(cnt, n, bsum);
-  k_bin_scatter<<<pb, 256, 0, s>>>(X, np, g.invh, g.N, cnt, perm);
+  k_bin_scatter<<<pb, 256, 0, s>>>(X, np, g.invh, g.N1, g.N2, g.N3, cnt, perm);
   return cudaGetLastError();
 }
 

@@ -50,14 +50,16 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
            const long long *dev_n, long long n) {
   using K = XT<N>;
   constexpr int M = K::M, RB = K::RB, T = K::T, LD = K::LD, NTG = K::NTG, G = K::G;
-  constexpr int S = K::SI_STAGES, NYB = N / RB;
+  constexpr int S = K::SI_STAGES;
+  const int N2 = g.N2, N3 = g.N3, NYB = N2 / RB;      // N = N1 (row length)
+  const int lgy = __ffs(NYB) - 1;                      // NYB is a power of two
   extern __shared__ __align__(1024) double2 smraw[];
   __shared__ uint64_t full[S], done[S];
   __shared__ int bad_any[G];
   double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
   constexpr size_t SW = K::SI / 16;
-  const int ntiles = N * NYB;
-  const size_t V = (size_t)N * N * N;
+  const int ntiles = N3 * NYB;
+  const size_t V = (size_t)g.V;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
     fence_mbar_init();
@@ -73,11 +75,11 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
         const int s = i % S;
         if (i >= S) mbar_wait(&done[s], ((i / S) - 1) & 1);
-        const int z = tile / NYB, y0 = (tile % NYB) * RB;
+        const int z = tile >> lgy, y0 = (tile & (NYB - 1)) * RB;
         double2 *b = stage0 + (size_t)s * SW;            // [3][RB][M] then [3][RB] Nyquist
         mbar_expect_tx(&full[s], (uint32_t)(3 * RB * (M + 1) * 16));
         for (int c = 0; c < 3; ++c) {
-          const int r0 = (c * N + z) * N + y0;
+          const int r0 = (c * N3 + z) * N2 + y0;
           tma_load_2d(b + (size_t)c * RB * M, &map_main, 0, r0, &full[s]);
           tma_load_2d(b + (size_t)3 * RB * M + c * K::NQ, &map_nyq, 2 * M, r0, &full[s]);
         }
@@ -93,12 +95,12 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
   bool bad = false;
   for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G) {
     const int s = i % S;
-    const int z = tile / NYB, y0 = (tile % NYB) * RB;
+    const int z = tile >> lgy, y0 = (tile & (NYB - 1)) * RB;
     double2 *sm = stage0 + (size_t)s * SW;
     const double2 *in = sm + (size_t)(comp * RB + row) * M;
     mbar_wait(&full[s], (i / S) & 1);
     const double2 nyq = sm[(size_t)3 * RB * M + comp * K::NQ + row];
-    double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * N + (y0 + row)) * N);
+    double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * N2 + (y0 + row)) * N);
     auto ld = [&](int e) -> double2 {
       double2 Xk = in[e], Xm = e == 0 ? nyq : in[M - e];
       if (e == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real
@@ -158,15 +160,14 @@ static int xt_rb(int N) {
   }
 }
 
-bool xpass_supported(int N) { return N >= 64 && N <= 256; }
+bool xpass_supported(int N) { return N >= 64 && N <= 256; }   // N = N1
 
 bool xpass_encode_s1(const FluidGeom &g, const double2 *spec, XMapsS *m) {
-  const int N = g.N;
-  if (!xpass_supported(N)) return false;
-  return encode_rows(&m->main, spec, (uint64_t)3 * N * N, 2 * (g.M + 1), (uint64_t)g.P * 16, N,
-                     xt_rb(N)) &&
-         encode_rows(&m->nyq, spec, (uint64_t)3 * N * N, 2 * (g.M + 1), (uint64_t)g.P * 16, 2,
-                     xt_rb(N));
+  const int N = g.N1;
+  if (!xpass_supported(N) || g.N2 % xt_rb(N)) return false;
+  const uint64_t rows = (uint64_t)3 * g.N2 * g.N3;
+  return encode_rows(&m->main, spec, rows, 2 * (g.M + 1), (uint64_t)g.P * 16, N, xt_rb(N)) &&
+         encode_rows(&m->nyq, spec, rows, 2 * (g.M + 1), (uint64_t)g.P * 16, 2, xt_rb(N));
 }
 
 template <class Kern>
@@ -192,7 +193,7 @@ static cudaError_t xinv_n(const FluidGeom &g, const XMapsS &m, double *out, cons
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  const int grid = grid_for(k_xinv_tma<N>, K::NTHR, smem, N * (N / K::RB));
+  const int grid = grid_for(k_xinv_tma<N>, K::NTHR, smem, g.N3 * (g.N2 / K::RB));
   k_xinv_tma<N><<<grid, K::NTHR, smem, s>>>(g, m.main, m.nyq, out, twN, twM, flag, dev_n, n);
   return cudaGetLastError();
 }
@@ -200,7 +201,7 @@ static cudaError_t xinv_n(const FluidGeom &g, const XMapsS &m, double *out, cons
 cudaError_t launch_xinv_tma(const FluidGeom &g, const XMapsS &m, double *out,
                             const double2 *twN, const double2 *twM, long long *flag,
                             const long long *dev_n, long long n, cudaStream_t s) {
-  switch (g.N) {
+  switch (g.N1) {
     case 64: return xinv_n<64>(g, m, out, twN, twM, flag, dev_n, n, s);
     case 128: return xinv_n<128>(g, m, out, twN, twM, flag, dev_n, n, s);
     case 256: return xinv_n<256>(g, m, out, twN, twM, flag, dev_n, n, s);

@@ -19,7 +19,7 @@ IB_OK, IB_EINVAL, IB_ENOMEM, IB_ECUDA, IB_ENONFINITE, IB_ESTATE, IB_EDEGENERATE 
 IB_WRAP1, IB_WRAP2, IB_STRETCH1, IB_STRETCH2, IB_BEND1, IB_BEND2, IB_TETHER = 1, 2, 4, 8, 16, 32, 64
 IB_OPT_PRESSURE, IB_OPT_STAGE_TIMING, IB_OPT_GRAPH = 1, 2, 3
 
-EXPORTS = ("ib_create", "ib_destroy", "ib_set_stream", "ib_set_option", "ib_set_structure",
+EXPORTS = ("ib_create", "ib_create3", "ib_destroy", "ib_set_stream", "ib_set_option", "ib_set_structure",
            "ib_set_positions", "ib_set_velocity", "ib_set_drive", "ib_step", "ib_get_fields",
            "ib_get_positions", "ib_get_step", "ib_set_step", "ib_num_points", "ib_stage_times",
            "ib_launch_count", "ib_last_error", "ib_debug_force", "ib_debug_spread",
@@ -57,6 +57,8 @@ def load(path: Optional[str] = None):
     p, d, i32, i64 = C.c_void_p, C.c_double, C.c_int32, C.c_int64
     L.ib_create.restype = p
     L.ib_create.argtypes = [i32, d, d, d, d]
+    L.ib_create3.restype = p
+    L.ib_create3.argtypes = [i32, i32, i32, d, d, d, d]
     L.ib_destroy.argtypes = [p]
     L.ib_set_stream.argtypes = [p, p]
     L.ib_set_option.argtypes = [p, i32, i64]
@@ -83,7 +85,7 @@ def load(path: Optional[str] = None):
     L.ib_debug_fluid.argtypes = [p, p, p, p, p]
     L.ib_debug_fft.argtypes = [p, p, p]
     for name in EXPORTS:
-        if name not in ("ib_create", "ib_destroy", "ib_get_step", "ib_num_points",
+        if name not in ("ib_create", "ib_create3", "ib_destroy", "ib_get_step", "ib_num_points",
                         "ib_launch_count", "ib_last_error"):
             getattr(L, name).restype = C.c_int
     _lib = L
@@ -119,8 +121,22 @@ def _ptr(a, dtype=np.float64, size: Optional[int] = None, writable=False):
 
 
 # ------------------------------------------------------------------ C-named functions
+def dims(N):
+    """(N1, N2, N3) from an int (cubic lattice) or a 3-sequence (x, y, z)."""
+    if isinstance(N, (tuple, list)):
+        return tuple(int(v) for v in N)
+    return int(N), int(N), int(N)
+
+
 def ib_create(N: int, h: float, rho: float, mu: float, dt: float) -> int:
     ctx = load().ib_create(int(N), float(h), float(rho), float(mu), float(dt))
+    if not ctx:
+        raise IBError(IB_EINVAL, load().ib_last_error().decode())
+    return ctx
+
+
+def ib_create3(N1: int, N2: int, N3: int, h: float, rho: float, mu: float, dt: float) -> int:
+    ctx = load().ib_create3(int(N1), int(N2), int(N3), float(h), float(rho), float(mu), float(dt))
     if not ctx:
         raise IBError(IB_EINVAL, load().ib_last_error().decode())
     return ctx
@@ -157,8 +173,9 @@ def ib_set_positions(ctx, points) -> None:
     _check(load().ib_set_positions(ctx, _ptr(points, size=3 * load().ib_num_points(ctx))))
 
 
-def ib_set_velocity(ctx, u, N: int) -> None:
-    _check(load().ib_set_velocity(ctx, _ptr(u, size=3 * N ** 3)))
+def ib_set_velocity(ctx, u, N) -> None:
+    n1, n2, n3 = dims(N)
+    _check(load().ib_set_velocity(ctx, _ptr(u, size=3 * n1 * n2 * n3)))
 
 
 def ib_set_drive(ctx, idx, direction, amp_per_point: float, period_steps: int) -> None:
@@ -172,8 +189,9 @@ def ib_step(ctx, nsteps: int) -> None:
     _check(load().ib_step(ctx, int(nsteps)))
 
 
-def ib_get_fields(ctx, u_out=None, p_out=None, N: int = None) -> None:
-    V = N ** 3
+def ib_get_fields(ctx, u_out=None, p_out=None, N=None) -> None:
+    n1, n2, n3 = dims(N)
+    V = n1 * n2 * n3
     _check(load().ib_get_fields(ctx, _ptr(u_out, size=3 * V, writable=True),
                                 _ptr(p_out, size=V, writable=True)))
 
@@ -206,12 +224,28 @@ def ib_launch_count(ctx, reset: bool = False) -> int:
 
 # ------------------------------------------------------------------ convenience object
 class IBContext:
-    """Owning wrapper: `IBContext(N, h, rho, mu, dt)` + the ib_* calls as methods."""
+    """Owning wrapper: `IBContext(N, h, rho, mu, dt)` + the ib_* calls as methods.  N is an
+    int (N^3 lattice, ib_create) or (N1, N2, N3) (ib_create3); fields are [3][N3][N2][N1]."""
 
     def __init__(self, N, h, rho, mu, dt):
-        self.N, self.h, self.rho, self.mu, self.dt = int(N), float(h), float(rho), float(mu), float(dt)
-        self.ctx = ib_create(N, h, rho, mu, dt)
+        self.dims = dims(N)
+        self.N = self.dims if isinstance(N, (tuple, list)) else int(N)
+        self.h, self.rho, self.mu, self.dt = float(h), float(rho), float(mu), float(dt)
+        if isinstance(N, (tuple, list)):
+            self.ctx = ib_create3(*self.dims, h, rho, mu, dt)
+        else:
+            self.ctx = ib_create(N, h, rho, mu, dt)
         self.np = 0
+
+    @property
+    def fshape(self):
+        n1, n2, n3 = self.dims
+        return (3, n3, n2, n1)
+
+    @property
+    def V(self):
+        n1, n2, n3 = self.dims
+        return n1 * n2 * n3
 
     @classmethod
     def from_config(cls, cfg):
@@ -251,7 +285,7 @@ class IBContext:
         ib_set_positions(self.ctx, np.ascontiguousarray(X, dtype=np.float64) if isinstance(X, np.ndarray) else X)
 
     def set_velocity(self, u):
-        ib_set_velocity(self.ctx, np.ascontiguousarray(u, dtype=np.float64) if isinstance(u, np.ndarray) else u, self.N)
+        ib_set_velocity(self.ctx, np.ascontiguousarray(u, dtype=np.float64) if isinstance(u, np.ndarray) else u, self.dims)
 
     def set_drive(self, idx, direction, amp, period):
         ib_set_drive(self.ctx, np.ascontiguousarray(idx, dtype=np.int64),
@@ -274,14 +308,13 @@ class IBContext:
         ib_set_step(self.ctx, n)
 
     def get_fields(self, want_p=False):
-        N = self.N
-        u = np.empty((3, N, N, N))
-        p = np.empty((N, N, N)) if want_p else None
-        ib_get_fields(self.ctx, u, p, N)
+        u = np.empty(self.fshape)
+        p = np.empty(self.fshape[1:]) if want_p else None
+        ib_get_fields(self.ctx, u, p, self.dims)
         return u, p
 
     def get_fields_into(self, u_out=None, p_out=None):
-        ib_get_fields(self.ctx, u_out, p_out, self.N)
+        ib_get_fields(self.ctx, u_out, p_out, self.dims)
 
     def get_positions(self):
         X = np.empty((self.np, 3))
@@ -304,39 +337,36 @@ class IBContext:
         return out
 
     def debug_spread(self, f_node):
-        N = self.N
         f = np.ascontiguousarray(f_node, dtype=np.float64)
-        F = np.empty((3, N, N, N))
+        F = np.empty(self.fshape)
         _check(load().ib_debug_spread(self.ctx, _ptr(f, size=3 * self.np), _ptr(F)))
         return F
 
     def debug_interp(self, u):
         u = np.ascontiguousarray(u, dtype=np.float64)
         U = np.empty((self.np, 3))
-        _check(load().ib_debug_interp(self.ctx, _ptr(u, size=3 * self.N ** 3), _ptr(U)))
+        _check(load().ib_debug_interp(self.ctx, _ptr(u, size=3 * self.V), _ptr(U)))
         return U
 
     def debug_rhs(self, u, F):
-        N = self.N
         u = np.ascontiguousarray(u, dtype=np.float64)
         F = np.ascontiguousarray(F, dtype=np.float64)
-        r = np.empty((3, N, N, N))
-        _check(load().ib_debug_rhs(self.ctx, _ptr(u, size=3 * N ** 3), _ptr(F, size=3 * N ** 3), _ptr(r)))
+        r = np.empty(self.fshape)
+        _check(load().ib_debug_rhs(self.ctx, _ptr(u, size=3 * self.V), _ptr(F, size=3 * self.V), _ptr(r)))
         return r
 
     def debug_fluid(self, u, F, want_p=True):
-        N = self.N
         u = np.ascontiguousarray(u, dtype=np.float64)
         F = np.ascontiguousarray(F, dtype=np.float64)
-        un = np.empty((3, N, N, N))
-        p = np.empty((N, N, N)) if want_p else None
-        _check(load().ib_debug_fluid(self.ctx, _ptr(u, size=3 * N ** 3), _ptr(F, size=3 * N ** 3),
+        un = np.empty(self.fshape)
+        p = np.empty(self.fshape[1:]) if want_p else None
+        _check(load().ib_debug_fluid(self.ctx, _ptr(u, size=3 * self.V), _ptr(F, size=3 * self.V),
                                      _ptr(un), _ptr(p)))
         return un, p
 
     def debug_fft(self, x):
-        N = self.N
+        n1, n2, n3 = self.dims
         x = np.ascontiguousarray(x, dtype=np.float64)
-        out = np.empty((N, N, N // 2 + 1, 2))
-        _check(load().ib_debug_fft(self.ctx, _ptr(x, size=N ** 3), _ptr(out)))
+        out = np.empty((n3, n2, n1 // 2 + 1, 2))
+        _check(load().ib_debug_fft(self.ctx, _ptr(x, size=self.V), _ptr(out)))
         return out[..., 0] + 1j * out[..., 1]

@@ -280,3 +280,78 @@ def test_config_full_length_stays_finite_and_bounded(ibm, k):
     dmax = float(np.max(np.abs(X - cfg.X)))
     print(f"cfg{k}: {cfg.steps} steps, max|u| {umax:.3e}, max|X-X0| {dmax:.3e}")
     assert umax < 100.0 and dmax < 0.5 * cfg.N * cfg.h
+
+
+# ---------------------------------------------------------------- anisotropic lattices
+# N1 x N2 x N3 boxes such as the paper's 256 x 256 x 128 half-cube
+# (PAPER.md 1003-1007).  Shapes mix the TMA column passes (pencil >= 64) with the cp.async
+# pencil kernels (pencil < 64) on each axis.
+ANISO = [(32, 64, 16), (64, 32, 128), (16, 16, 64), (128, 64, 32)]
+
+
+@pytest.mark.parametrize("shape", ANISO)
+def test_fft_anisotropic(ibm, shape):
+    n1, n2, n3 = shape
+    x = np.random.default_rng(n1 + n2 + n3).standard_normal((n3, n2, n1))
+    with ibm.IBContext(shape, 1.0 / n1, 1.0, 0.01, 1e-3) as c:
+        got = c.debug_fft(x)
+    ref = np.fft.rfftn(x)
+    assert got.shape == ref.shape
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref)) * np.log2(n1 * n2 * n3)
+
+
+@pytest.mark.parametrize("shape", ANISO)
+def test_fluid_step_anisotropic(ibm, olib, shape):
+    n1, n2, n3 = shape
+    rng = np.random.default_rng(31)
+    h = 1.0 / n1
+    u = random_divfree_velocity(shape, 3, 0.3, rng) + 0.05 * rng.standard_normal((3, n3, n2, n1))
+    F = rng.standard_normal((3, n3, n2, n1)) * 50
+    rho, mu, dt = 1.0, 0.02, 1e-3
+    with ibm.IBContext(shape, h, rho, mu, dt) as c:
+        un, p = c.debug_fluid(u, F)
+        r = c.debug_rhs(u, F)
+    ref_u, ref_p = olib.fluid_step(shape, h, rho, mu, dt, u, F)
+    assert rel_l2(r, olib.rhs(shape, h, rho, dt, u, F)) < 1e-14
+    assert rel_l2(un, ref_u) < 1e-13
+    assert rel_l2(p, ref_p) < 1e-12
+
+
+@pytest.mark.parametrize("shape", [(32, 64, 16), (64, 32, 128)])
+def test_spread_interp_anisotropic(ibm, olib, shape):
+    n1, n2, n3 = shape
+    h = 1.0 / n1
+    rng = np.random.default_rng(32)
+    L = np.array(shape) * h
+    centres = rng.uniform(-0.2, 1.2, (60, 3)) * L
+    X = centres[rng.integers(0, 60, 6000)] + rng.uniform(0, 0.4 * h, (6000, 3))
+    f = rng.standard_normal((6000, 3))
+    u = rng.standard_normal((3, n3, n2, n1))
+    patches, st = _points_only(X)
+    with ibm.IBContext(shape, h, 1.0, 0.01, 1e-3) as c:
+        c.set_structure(X, patches, st)
+        F = c.debug_spread(f)
+        U = c.debug_interp(u)
+    assert rel_l2(F, olib.spread(shape, h, X, f)) < 1e-13
+    assert rel_l2(U, olib.interp(shape, h, u, X)) < 1e-14
+
+
+@pytest.mark.parametrize("shape", [(32, 64, 16), (64, 64, 128)])
+def test_step_parity_anisotropic_with_pressure_every_step(ibm, olib, shape):
+    """Full IB steps on an anisotropic box (sheet with all link families, tethers, drive,
+    flow), and the pressure of EVERY step: ib_step(1) + ib_get_fields(p) per step against
+    the oracle's per-step pressure history."""
+    cfg = small_sheet_config(N=shape, n1=20, n2=14, seed=33, u_amp=0.2)
+    o = olib.Oracle.from_config(cfg)
+    with ibm.IBContext.from_config(cfg) as c:
+        c.set_option(ibm.IB_OPT_PRESSURE, 1)
+        ps = []
+        for _ in range(4):
+            c.step(1)
+            ps.append(c.get_fields(want_p=True)[1])
+        o.step(4, p_every=True)
+        ug, _ = c.get_fields()
+        Xg = c.get_positions()
+    assert rel_l2(ug, o.u) < 1e-11 and rel_l2(Xg, o.X) < 1e-11
+    for k in range(4):
+        assert rel_l2(ps[k], o.p_steps[k]) < 1e-10, k
