@@ -32,11 +32,22 @@ UNIT = "steps/s"
 
 
 # ------------------------------------------------------------------ algorithmic bytes
-def stage_bytes(N: int, np_: int, nd: int = 0) -> dict:
-    """Compulsory HBM bytes per launch of each stage (DESIGN.md §6 byte model).
-    V = N^3 cells, C = N^2 (N/2+1) complex modes per component."""
-    V = N ** 3
-    C = N * N * (N // 2 + 1)
+def dims(N):
+    """(N1, N2, N3) from an int (cubic lattice) or a 3-sequence (x, y, z)."""
+    return tuple(int(v) for v in N) if isinstance(N, (tuple, list)) else (int(N),) * 3
+
+
+def grid_name(N) -> str:
+    n1, n2, n3 = dims(N)
+    return f"{n1}^3" if n1 == n2 == n3 else f"{n1}x{n2}x{n3}"
+
+
+def stage_bytes(N, np_: int, nd: int = 0) -> dict:
+    """Compulsory HBM bytes per launch of each stage (DESIGN.md §5 byte model).
+    V = N1 N2 N3 cells, C = N2 N3 (N1/2+1) complex modes per component."""
+    n1, n2, n3 = dims(N)
+    V = n1 * n2 * n3
+    C = n2 * n3 * (n1 // 2 + 1)
     return {
         # X (24) + neighbour X (24, cached) + per-point k/L0 (32) -> 80 B/pt; F band RMW
         # is on-chip (L2 atomics) and not counted
@@ -203,7 +214,7 @@ def run_reference(args, ws, rank):
     o.step(k)
     dt = time.perf_counter() - t0
     v = k / dt
-    sample = f"{k} full IB steps of cfg{args.config} ({cfg.N}^3, {cfg.np_} points) after {w} warm-up"
+    sample = f"{k} full IB steps of cfg{args.config} ({grid_name(cfg.N)}, {cfg.np_} points) after {w} warm-up"
     line = {"metric": METRIC, "value": v, "unit": UNIT, "impl": "reference", "n_gpus": ws,
             "steps": k, "warmup": w, "ms_per_step": 1e3 * dt / k, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -216,11 +227,14 @@ def run_reference(args, ws, rank):
 
 
 def workload_config(cfg, k):
-    return {"workload": f"BASELINE.json configs[{k - 1}] ({cfg.name}): {cfg.N}^3 periodic grid, "
+    src = (f"BASELINE.json configs[{int(k) - 1}]" if k != "4h" else
+           "half-cube variant of BASELINE.json configs[3] (PAPER.md 1003-1007)")
+    return {"workload": f"{src} ({cfg.name}): {grid_name(cfg.N)} periodic grid, "
                         f"{cfg.np_} Lagrangian points",
-            "N": cfg.N, "lagrangian_points": cfg.np_, "global_batch": 1,
+            "N": cfg.N if isinstance(cfg.N, int) else list(cfg.N),
+            "lagrangian_points": cfg.np_, "global_batch": 1,
             "parallelism": "replicas", "l2": "inputs larger than L2 (u + spectrum >> 126 MB)"
-            if cfg.N >= 256 else "working set fits in L2 (no flush)"}
+            if np.prod(dims(cfg.N)) >= 128 ** 3 * 4 else "working set fits in L2 (no flush)"}
 
 
 # ------------------------------------------------------------------ our arm
@@ -293,7 +307,8 @@ def run_ours(args, ws, rank, local):
     # end-to-end through the C-ABI with pinned host buffers: per step H2D (u, X), step,
     # D2H (u, X)
     ke = max(2, min(args.steps, args.e2e_steps))
-    hu = torch.empty((3, N, N, N), dtype=torch.float64).pin_memory()
+    n1, n2, n3 = dims(N)
+    hu = torch.empty((3, n3, n2, n1), dtype=torch.float64).pin_memory()
     hX = torch.empty((npts, 3), dtype=torch.float64).pin_memory()
     ctx.get_fields_into(hu)
     ctx.get_positions_into(hX)
@@ -301,7 +316,7 @@ def run_ours(args, ws, rank, local):
     barrier()
     t0 = time.perf_counter()
     for _ in range(ke):
-        ibmod.ib_set_velocity(ctx.ctx, hu, N)
+        ibmod.ib_set_velocity(ctx.ctx, hu, dims(N))
         ibmod.ib_set_positions(ctx.ctx, hX)
         ctx.step(1)
         ctx.get_fields_into(hu)
@@ -325,7 +340,7 @@ def run_ours(args, ws, rank, local):
                 "dtype": "f64", "data": "synthetic", "config": workload_config(cfg, args.config),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": launches,
-                "throughput": {"cells_per_s": value * N ** 3, "points_per_s": value * npts},
+                "throughput": {"cells_per_s": value * int(np.prod(dims(N))), "points_per_s": value * npts},
                 "stages": per_stage}
         print(json.dumps(line), flush=True)
     return 0
@@ -345,7 +360,7 @@ def cpu_baseline(args):
         k += 1
     dt = time.perf_counter() - t0
     return {"value": k / dt, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
-            "sample": f"{k} full IB steps of cfg{args.config} ({cfg.N}^3, {cfg.np_} points), "
+            "sample": f"{k} full IB steps of cfg{args.config} ({grid_name(cfg.N)}, {cfg.np_} points), "
                       f"{dt:.1f} s"}
 
 
@@ -354,7 +369,7 @@ def main(argv=None):
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--config", default="4", help="1..5 (BASELINE.json configs) or 4h (half-cube)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -171,14 +171,15 @@ def random_divfree_velocity(N, K: int, amplitude: float, rng: np.random.Generato
 
 
 # --------------------------------------------------------------------------- geometry
-def _helix(n1: int):
-    """Centre-line C(theta), frame (t, n, e) of the 2.5-turn helix (BASELINE.json cfg3)."""
+def _helix(n1: int, th_max: float = 5.0 * math.pi, z0: float = 0.35):
+    """Centre-line C(theta), frame (t, n, e) of the helix of BASELINE.json cfg3: theta in
+    [0, th_max] (2.5 turns by default), radius 0.35 -> 0.1, pitch 0.12, starting at z0."""
     i = np.arange(n1, dtype=np.float64)
-    th = 5.0 * math.pi * i / (n1 - 1)
-    R = 0.35 - 0.25 * th / (5.0 * math.pi)
-    dR = -0.25 / (5.0 * math.pi)
+    th = th_max * i / (n1 - 1)
+    R = 0.35 - 0.25 * th / th_max
+    dR = -0.25 / th_max
     C = np.stack([0.5 + R * np.cos(th), 0.5 + R * np.sin(th),
-                  0.35 + 0.12 * th / (2.0 * math.pi)], axis=-1)
+                  z0 + 0.12 * th / (2.0 * math.pi)], axis=-1)
     dC = np.stack([dR * np.cos(th) - R * np.sin(th), dR * np.sin(th) + R * np.cos(th),
                    np.full_like(th, 0.12 / (2.0 * math.pi))], axis=-1)
     t = dC / np.linalg.norm(dC, axis=-1, keepdims=True)
@@ -189,8 +190,8 @@ def _helix(n1: int):
     return C, t, n, e
 
 
-def _strip(n1: int, n2: int):
-    C, t, n, e = _helix(n1)
+def _strip(n1: int, n2: int, **hx):
+    C, t, n, e = _helix(n1, **hx)
     i = np.arange(n1, dtype=np.float64)
     w = 0.01 + 0.03 * i / (n1 - 1)
     j = np.arange(n2, dtype=np.float64)
@@ -199,8 +200,8 @@ def _strip(n1: int, n2: int):
     return np.ascontiguousarray(P), n
 
 
-def _walls(n1: int, n2: int, a: float = 0.045):
-    C, t, n, e = _helix(n1)
+def _walls(n1: int, n2: int, a: float = 0.045, **hx):
+    C, t, n, e = _helix(n1, **hx)
     out = []
     for base in (0.0, math.pi):
         psi = base + math.pi * (np.arange(n2, dtype=np.float64) + 0.5) / n2
@@ -287,9 +288,9 @@ def _cfg2() -> Config:
 
 
 def _helix_config(name, N, mu, dt, steps, n1, n2, nw2, walls: bool, jitter_rng=None,
-                  u0=None) -> Config:
-    h = 1.0 / N
-    P, nrm = _strip(n1, n2)
+                  u0=None, **hx) -> Config:
+    h = 1.0 / _dims(N)[0]
+    P, nrm = _strip(n1, n2, **hx)
     flags = STRETCH1 | STRETCH2
     s = np.arange(n1, dtype=np.float64) / (n1 - 1)
     kprof = np.broadcast_to(100.0 ** (-s)[None, :], (n2, n1))        # reading Z2
@@ -297,7 +298,7 @@ def _helix_config(name, N, mu, dt, steps, n1, n2, nw2, walls: bool, jitter_rng=N
     for fam, axis, off in FAMILIES[:2]:
         L0 = _rest_lengths(P, n1, n2, axis, off, False)
         blocks += [np.where(L0 > 0, kprof, 0.0), L0]
-    wall_P = _walls(n1, nw2) if walls else []
+    wall_P = _walls(n1, nw2, **hx) if walls else []
     kt = []
     for W in wall_P:
         dA = _spacing(W, 1) * _spacing(W, 0)
@@ -335,12 +336,21 @@ def _cfg5() -> Config:
                          jitter_rng=rng, u0=u0)
 
 
-_MAKERS = {1: _cfg1, 2: _cfg2, 3: _cfg3, 4: _cfg4, 5: _cfg5}
+def _cfg4h() -> Config:
+    """The paper's half-cube box (256 x 256 x 128, PAPER.md 1003-1007) with
+    cfg4's physics and mesh sizes: strip 8192 x 64 and two tethered duct walls 8192 x 96
+    (2,097,152 points) on a 1.25-turn helix of the same radius law and pitch, starting at
+    z = 0.125 so that it fits the [0, 1) x [0, 1) x [0, 0.5) domain."""
+    return _helix_config("cfg4h", (256, 256, 128), 1e-3, 1.25e-4, 200, 8192, 64, 96, True,
+                         th_max=2.5 * math.pi, z0=0.125)
 
 
-def make_config(k: int) -> Config:
-    """BASELINE.json configs[k-1] as arrays (k = 1..5)."""
-    return _MAKERS[k]()
+_MAKERS = {1: _cfg1, 2: _cfg2, 3: _cfg3, 4: _cfg4, 5: _cfg5, "4h": _cfg4h}
+
+
+def make_config(k) -> Config:
+    """BASELINE.json configs[k-1] as arrays (k = 1..5); k = "4h": the half-cube variant."""
+    return _MAKERS[k if k == "4h" else int(k)]()
 
 
 # --------------------------------------------------------------------------- small cases

@@ -355,3 +355,9 @@ def test_step_parity_anisotropic_with_pressure_every_step(ibm, olib, shape):
     assert rel_l2(ug, o.u) < 1e-11 and rel_l2(Xg, o.X) < 1e-11
     for k in range(4):
         assert rel_l2(ps[k], o.p_steps[k]) < 1e-10, k
+
+
+@pytest.mark.slow
+def test_halfcube_step_parity(ibm, olib):
+    """The 256 x 256 x 128 half-cube workload (gen make_config("4h")): 1 + 9 steps."""
+    print(_parity(ibm, olib, make_config("4h")))
