@@ -58,6 +58,7 @@ class Config:
     drive_dir: Optional[np.ndarray] = None   # float64 [nd][3]
     drive_amp: float = 0.0             # amplitude per driven point
     drive_period: int = 1              # steps
+    fixed: Optional[np.ndarray] = None  # uint8 [np]: 1 = point never moves (window plates)
     info: dict = field(default_factory=dict)
 
     @property
@@ -400,4 +401,48 @@ def small_sheet_config(N=16, n1: int = 12, n2: int = 10, seed: int = 0,
         cfg.drive_dir = np.ascontiguousarray(d / np.linalg.norm(d, axis=1, keepdims=True))
         cfg.drive_amp = 0.05
         cfg.drive_period = 8
+    return cfg
+
+
+def window_config(N=32, m: int = 24, seed: int = 0, rho: float = 1.0, mu: float = 0.01,
+                  dt: float = 1e-3, amp: float = 2e-3, period: int = 8, k: float = 1.0,
+                  u_amp: float = 0.0) -> Config:
+    """An oval-window-like plate (PAPER.md 914-922, 988-993): an m x m
+    rectangular grid at spacing h/2 with stretch links of uniform stiffness k, tilted out of
+    the lattice planes; its points outside the inscribed circle are fixed (a circular plate
+    in a rectangular piece of bone); a sinusoidal force of total amplitude `amp` orthogonal
+    to the plate surface (the normal recomputed from X^n each step) is distributed uniformly
+    over the free disc points.  Rest lengths are the initial spacings, and the disc starts
+    bulged by a seeded random normal displacement so that the plate is stressed."""
+    rng = np.random.default_rng(seed)
+    h = 1.0 / _dims(N)[0]
+    s = h / 2
+    e1 = np.array([0.96, 0.28, 0.0])
+    e2 = np.array([-0.1, 0.35, 0.93])
+    e2 -= e1 * (e1 @ e2); e2 /= np.linalg.norm(e2)
+    nrm = np.cross(e1, e2)
+    i1 = np.arange(m, dtype=np.float64)[None, :, None]
+    i2 = np.arange(m, dtype=np.float64)[:, None, None]
+    c = (m - 1) / 2.0
+    P = 0.47 + (i1 - c) * s * e1 + (i2 - c) * s * e2                 # [m][m][3]
+    rr = np.sqrt((i1[..., 0] - c) ** 2 + (i2[..., 0] - c) ** 2)     # [m][m]
+    disc = rr <= c
+    flags = STRETCH1 | STRETCH2
+    blocks = []
+    for fam, axis, off in FAMILIES[:2]:
+        L0 = _rest_lengths(np.ascontiguousarray(P), m, m, axis, off, False)
+        blocks += [np.where(L0 > 0, k, 0.0), L0]
+    bulge = 0.15 * h * rng.standard_normal((m, m)) * disc
+    P = np.ascontiguousarray(P + bulge[..., None] * nrm)
+    b = _Builder()
+    b.add(P, flags, blocks)
+    X, S = b.arrays()
+    u0 = random_divfree_velocity(N, 3, u_amp, rng) if u_amp > 0 else None
+    name = "window" + ("x".join(str(v) for v in N) if isinstance(N, (tuple, list)) else str(N))
+    cfg = Config(name, N, h, rho, mu, dt, 10, X, b.patches, S, u0=u0)
+    cfg.fixed = np.ascontiguousarray((~disc).reshape(-1).astype(np.uint8))
+    cfg.drive_idx = np.flatnonzero(disc.reshape(-1)).astype(np.int64)
+    cfg.drive_dir = None                                     # surface-normal drive
+    cfg.drive_amp = amp / cfg.drive_idx.size
+    cfg.drive_period = period
     return cfg

@@ -100,10 +100,18 @@ int ib_set_structure(ib_ctx *ctx, const double *points, int64_t np, const ib_pat
 int ib_set_positions(ib_ctx *ctx, const double *points);
 /* Fluid velocity u^n, [3][N3][N2][N1]. */
 int ib_set_velocity(ib_ctx *ctx, const double *u);
-/* External drive (PAPER.md 988-993, simplified): F_idx[d] += amp * sin(2 pi n / period) *
- * dir[d] at step n (t^n = n dt).  n = 0 clears the drive. */
+/* External drive (PAPER.md 988-993): F_idx[d] += amp * sin(2 pi n / period) * dir[d] at
+ * step n (t^n = n dt).  dir == NULL: surface-normal drive ("orthogonal to the surface of
+ * the window") — dir[d] is the unit normal t1 x t2 / |t1 x t2| of point idx[d]'s patch at
+ * X^n, with tangents t1, t2 the central differences along i1, i2 (one-sided at an open
+ * patch edge, periodic with IB_WRAP1/2); such points need a patch with n1, n2 >= 2.
+ * n = 0 clears the drive.  ib_set_structure clears it. */
 int ib_set_drive(ib_ctx *ctx, const int64_t *idx, int64_t n, const double *dir,
                  double amp_per_point, int32_t period_steps);
+/* Fixed points (window plates, PAPER.md 914-922: "a rectangular grid, all of whose points
+ * outside a given circle are fixed"): mask[np], mask[q] != 0 -> X(q) never moves; the point
+ * still exerts its link forces on the fluid.  NULL clears; ib_set_structure clears it. */
+int ib_set_fixed(ib_ctx *ctx, const uint8_t *mask);
 
 /* Advance nsteps time steps; synchronises the stream at the end.  Returns IB_ENONFINITE
  * (ib_last_error names the step) if u or X became non-finite. */

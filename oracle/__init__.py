@@ -56,7 +56,7 @@ def lib():
             L.ibo_fluid_step.argtypes = n3 + [d, d, d, d, p, p, p, p]
             L.ibo_step.restype = C.c_int
             L.ibo_step.argtypes = n3 + [d, d, d, d, p, p, p, i64, i32, p, p, p, p, p, p,
-                                        i64, p, p, d, i32, i64, i32, i32]
+                                        i64, p, p, d, i32, i64, i32, i32, p]
             _lib = L
     return _lib
 
@@ -123,7 +123,7 @@ def force(X, patches, stiffness, step=0, drive_idx=None, drive_dir=None, drive_a
     S = _Structure(patches, stiffness)
     nd = 0 if drive_idx is None else len(drive_idx)
     di = np.ascontiguousarray(drive_idx, dtype=np.int64) if nd else None
-    dd = _f64(drive_dir, (-1, 3)) if nd else None
+    dd = _f64(drive_dir, (-1, 3)) if (nd and drive_dir is not None) else None   # None: normal
     out = np.zeros_like(X)
     lib().ibo_force(_ptr(X), X.shape[0], *S.args(), nd, _ptr(di), _ptr(dd), float(drive_amp),
                     int(drive_period), int(step), _ptr(out))
@@ -200,6 +200,7 @@ class Oracle:
         self.nd = 0
         self.di = self.dd = None
         self.amp, self.period = 0.0, 1
+        self.fixed = None                # uint8 [np] or None
         self.n = 0
 
     @classmethod
@@ -210,6 +211,8 @@ class Oracle:
             o.set_velocity(cfg.u0)
         if cfg.drive_idx is not None:
             o.set_drive(cfg.drive_idx, cfg.drive_dir, cfg.drive_amp, cfg.drive_period)
+        if getattr(cfg, "fixed", None) is not None:
+            o.set_fixed(cfg.fixed)
         return o
 
     def set_structure(self, X, patches, stiffness):
@@ -223,10 +226,14 @@ class Oracle:
         self.u = _f64(u, fshape(self.dims)).copy()
 
     def set_drive(self, idx, direction, amp, period):
+        """direction None: surface-normal drive (normal of each point's patch at X^n)."""
         self.nd = len(idx)
         self.di = np.ascontiguousarray(idx, dtype=np.int64)
-        self.dd = _f64(direction, (-1, 3))
+        self.dd = None if direction is None else _f64(direction, (-1, 3))
         self.amp, self.period = float(amp), int(period)
+
+    def set_fixed(self, mask):
+        self.fixed = None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8)
 
     def step(self, nsteps=1, p_every=False):
         """nsteps IB steps; p_every: keep p^{n+1} of every step in self.p_steps."""
@@ -234,7 +241,7 @@ class Oracle:
         st = lib().ibo_step(*self.dims, self.h, self.rho, self.mu, self.dt, _ptr(self.u),
                             _ptr(pbuf), _ptr(self.X), self.X.shape[0], *self.S.args(),
                             self.nd, _ptr(self.di), _ptr(self.dd), self.amp, self.period,
-                            self.n, int(nsteps), 1 if p_every else 0)
+                            self.n, int(nsteps), 1 if p_every else 0, _ptr(self.fixed))
         if p_every:
             self.p_steps = pbuf
             if nsteps:

@@ -61,6 +61,30 @@ static void spring(const double *X, int64_t i, int64_t j, double k, double L0, d
   Fi[2] += t * dz;
 }
 
+/* Unit normal of a structured patch at point (i1, i2) from the current positions (the
+ * window drive "orthogonal to the surface of the window", PAPER.md 988-993): tangents by
+ * central differences along i1 and i2 (one-sided at an open patch edge, periodic with the
+ * WRAP flags), n = t1 x t2 / |t1 x t2|. */
+static void patch_normal(const double *X, int64_t first, int32_t n1, int32_t n2, uint32_t fl,
+                         int32_t i1, int32_t i2, double nrm[3]) {
+  double t[2][3];
+  for (int a = 0; a < 2; ++a) {
+    const int32_t n = a == 0 ? n1 : n2, c = a == 0 ? i1 : i2;
+    const int wrap = (fl & (a == 0 ? IBO_WRAP1 : IBO_WRAP2)) != 0;
+    int32_t cp = c + 1, cm = c - 1;
+    if (wrap) { cp %= n; cm = (cm + n) % n; }
+    else { if (cp > n - 1) cp = n - 1; if (cm < 0) cm = 0; }
+    const int64_t jp = a == 0 ? (int64_t)i2 * n1 + cp : (int64_t)cp * n1 + i1;
+    const int64_t jm = a == 0 ? (int64_t)i2 * n1 + cm : (int64_t)cm * n1 + i1;
+    for (int d = 0; d < 3; ++d) t[a][d] = X[3 * (first + jp) + d] - X[3 * (first + jm) + d];
+  }
+  const double cx = t[0][1] * t[1][2] - t[0][2] * t[1][1];
+  const double cy = t[0][2] * t[1][0] - t[0][0] * t[1][2];
+  const double cz = t[0][0] * t[1][1] - t[0][1] * t[1][0];
+  const double len = sqrt((cx * cx + cy * cy) + cz * cz);
+  nrm[0] = cx / len; nrm[1] = cy / len; nrm[2] = cz / len;
+}
+
 void ibo_force(const double *X, int64_t np, int32_t npatch, const int64_t *first,
                const int32_t *n1v, const int32_t *n2v, const uint32_t *flagsv,
                const int64_t *param_off, const double *stiff,
@@ -117,9 +141,19 @@ void ibo_force(const double *X, int64_t np, int32_t npatch, const int64_t *first
     double s = drive_amp * sin(2.0 * PI * (double)(step % drive_period) / (double)drive_period);
     for (int64_t d = 0; d < nd; ++d) {
       int64_t i = drive_idx[d];
-      Fnode[3 * i + 0] += s * drive_dir[3 * d + 0];
-      Fnode[3 * i + 1] += s * drive_dir[3 * d + 1];
-      Fnode[3 * i + 2] += s * drive_dir[3 * d + 2];
+      double dir[3];
+      if (drive_dir) {
+        dir[0] = drive_dir[3 * d + 0]; dir[1] = drive_dir[3 * d + 1]; dir[2] = drive_dir[3 * d + 2];
+      } else {                          /* surface-normal drive: the normal of i's patch at X^n */
+        int32_t p = 0;
+        while (p + 1 < npatch && first[p + 1] <= i) ++p;
+        const int64_t li = i - first[p];
+        patch_normal(X, first[p], n1v[p], n2v[p], flagsv[p], (int32_t)(li % n1v[p]),
+                     (int32_t)(li / n1v[p]), dir);
+      }
+      Fnode[3 * i + 0] += s * dir[0];
+      Fnode[3 * i + 1] += s * dir[1];
+      Fnode[3 * i + 2] += s * dir[2];
     }
   }
 }
@@ -365,7 +399,8 @@ int ibo_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu
              const int32_t *n1, const int32_t *n2, const uint32_t *flags,
              const int64_t *param_off, const double *stiff, int64_t nd,
              const int64_t *drive_idx, const double *drive_dir, double drive_amp,
-             int32_t drive_period, int64_t step0, int32_t nsteps, int32_t p_every) {
+             int32_t drive_period, int64_t step0, int32_t nsteps, int32_t p_every,
+             const uint8_t *fixed) {
   const size_t V = (size_t)N1 * N2 * N3;
   double *Fn = (double *)malloc(sizeof(double) * 3 * (size_t)(np > 0 ? np : 1));
   double *U = (double *)malloc(sizeof(double) * 3 * (size_t)(np > 0 ? np : 1));
@@ -380,7 +415,9 @@ int ibo_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu
     double *ps = (p && (p_every || s == nsteps - 1)) ? p + (p_every ? (size_t)s * V : 0) : NULL;
     ibo_fluid_step(N1, N2, N3, h, rho, mu, dt, u, F, un, ps);           /* step 3 */
     ibo_interp(N1, N2, N3, h, un, X, np, U);                            /* step 4 */
-    for (int64_t i = 0; i < 3 * np; ++i) X[i] = X[i] + dt * U[i];       /* eq:discreteX */
+    for (int64_t q = 0; q < np; ++q)                                    /* eq:discreteX */
+      if (!(fixed && fixed[q]))                      /* fixed points never move (PAPER.md 919-920) */
+        for (int d = 0; d < 3; ++d) X[3 * q + d] = X[3 * q + d] + dt * U[3 * q + d];
     memcpy(u, un, sizeof(double) * 3 * V);
     for (int64_t i = 0; i < 3 * np && !status; ++i) if (!isfinite(X[i])) status = 1 + s;
     for (size_t i = 0; i < 3 * V && !status; ++i) if (!isfinite(u[i])) status = 1 + s;

@@ -32,7 +32,9 @@ int    ibo_get_threads(void);
 /* Peskin 4-point phi(r), PAPER.md lines 745-759 (written exactly as the paper states). */
 double ibo_phi(double r);
 
-/* Step 1 — nodal Lagrangian force f^n: springs, tethers, drive. */
+/* Step 1 — nodal Lagrangian force f^n: springs, tethers, drive.
+ * drive_dir == NULL: surface-normal drive (PAPER.md 988-993) — each driven point is pushed
+ * along the unit normal of its patch at X^n (central-difference tangents). */
 void ibo_force(const double *X, int64_t np, int32_t npatch, const int64_t *first,
                const int32_t *n1, const int32_t *n2, const uint32_t *flags,
                const int64_t *param_off, const double *stiff,
@@ -72,14 +74,16 @@ void ibo_fluid_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, do
 
 /* nsteps full IB steps.  u[3][V] and X[np][3] in/out; p (may be
  * NULL) receives p^{n+1}: of the last step ([V]) when p_every == 0, of every step
- * ([nsteps][V]) when p_every != 0.  Returns 0, or 1 + the 0-based step index at which a
- * non-finite value appeared. */
+ * ([nsteps][V]) when p_every != 0.  fixed (may be NULL): points with fixed[q] != 0 never
+ * move but still exert their force (window plates, PAPER.md 914-922).  Returns 0, or 1 +
+ * the 0-based step index at which a non-finite value appeared. */
 int ibo_step(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu, double dt,
              double *u, double *p, double *X, int64_t np, int32_t npatch, const int64_t *first,
              const int32_t *n1, const int32_t *n2, const uint32_t *flags,
              const int64_t *param_off, const double *stiff, int64_t nd,
              const int64_t *drive_idx, const double *drive_dir, double drive_amp,
-             int32_t drive_period, int64_t step0, int32_t nsteps, int32_t p_every);
+             int32_t drive_period, int64_t step0, int32_t nsteps, int32_t p_every,
+             const uint8_t *fixed);
 
 #ifdef __cplusplus
 }

@@ -190,7 +190,7 @@ cudaError_t enqueue_step(ib_ctx *c, bool pressure, cudaEvent_t *ev) {
   mark(5);
   if ((e = xinv(c, c->u, dev_n, n, c->flag, s)) != cudaSuccess) return e;
   mark(6);
-  if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, sd.perm, s)) != cudaSuccess) return e;
+  if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, sd.perm, c->fixed, s)) != cudaSuccess) return e;
   mark(7);
   return launch_step_inc(c->dev_n, s);
 }
@@ -322,7 +322,7 @@ void ib_destroy(ib_ctx *c) {
   for (int a = 0; a < 3; ++a) { dfree(c->tw[a]); dfree(c->sym_s[a]); dfree(c->sym_l[a]); }
   dfree(c->twM);
   dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->drive_idx); dfree(c->drive_dir);
-  dfree(c->perm); dfree(c->bincnt); dfree(c->binsum);
+  dfree(c->perm); dfree(c->bincnt); dfree(c->binsum); dfree(c->fixed);
   dfree(c->flag); dfree(c->dev_n);
   if (c->flag_h) cudaFreeHost(c->flag_h);
   for (int k = 0; k <= STAGE_COUNT; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
@@ -432,6 +432,8 @@ int ib_set_structure(ib_ctx *c, const double *points, int64_t np, const ib_patch
   c->np = np; c->npatch = npatch; c->nstiff = nstiff; c->patches_h = P;
   // a drive that no longer fits is dropped
   if (c->nd > 0) { dfree(c->drive_idx); dfree(c->drive_dir); c->drive_idx = nullptr; c->drive_dir = nullptr; c->nd = 0; }
+  dfree(c->fixed);                       // a fixed mask belongs to the old structure
+  c->fixed = nullptr;
   return IB_OK;
 }
 
@@ -465,32 +467,55 @@ int ib_set_drive(ib_ctx *c, const int64_t *idx, int64_t n, const double *dir,
   if (!c) return fail(IB_EINVAL, "ctx is NULL");
   if (n < 0) return fail(IB_EINVAL, "negative drive count");
   if (n > 0) {
-    if (!idx || !dir) return fail(IB_EINVAL, "NULL drive arrays");
+    if (!idx) return fail(IB_EINVAL, "NULL drive indices");
     if (period_steps < 1) return fail(IB_EINVAL, "period_steps must be >= 1");
     if (!std::isfinite(amp_per_point)) return fail(IB_EINVAL, "non-finite amplitude");
     std::vector<int64_t> I;
     std::vector<double> D;
     CK(to_host(I, idx, (size_t)n, c->stream));
-    CK(to_host(D, dir, (size_t)n * 3, c->stream));
+    if (dir) CK(to_host(D, dir, (size_t)n * 3, c->stream));
     for (int64_t d = 0; d < n; ++d) {
       if (I[d] < 0 || I[d] >= c->np) return fail(IB_EINVAL, "drive index out of range: " + std::to_string(I[d]));
-      for (int k = 0; k < 3; ++k)
-        if (!std::isfinite(D[3 * d + k])) return fail(IB_EINVAL, "non-finite drive direction");
+      if (dir) {
+        for (int k = 0; k < 3; ++k)
+          if (!std::isfinite(D[3 * d + k])) return fail(IB_EINVAL, "non-finite drive direction");
+      } else {                 // surface-normal drive: the point's patch must be a 2-D grid
+        int32_t p = 0;
+        while (p + 1 < c->npatch && c->patches_h[p + 1].first <= I[d]) ++p;
+        if (c->patches_h[p].n1 < 2 || c->patches_h[p].n2 < 2)
+          return fail(IB_EINVAL, "normal drive on point " + std::to_string(I[d]) +
+                                     " of a patch with n1 or n2 < 2 (no surface normal)");
+      }
     }
     free_graph(c);
     CK(cudaStreamSynchronize(c->stream));
     dfree(c->drive_idx); dfree(c->drive_dir);
     c->drive_idx = nullptr; c->drive_dir = nullptr;
     CK(dalloc(&c->drive_idx, (size_t)n));
-    CK(dalloc(&c->drive_dir, (size_t)n * 3));
     CK(copy_sync(c->drive_idx, I.data(), I.size() * sizeof(int64_t), c->stream));
-    CK(copy_sync(c->drive_dir, D.data(), D.size() * sizeof(double), c->stream));
+    if (dir) {
+      CK(dalloc(&c->drive_dir, (size_t)n * 3));
+      CK(copy_sync(c->drive_dir, D.data(), D.size() * sizeof(double), c->stream));
+    }
   } else {
     free_graph(c);
   }
   c->nd = n;
   c->drive_amp = amp_per_point;
   c->drive_period = n > 0 ? period_steps : 1;
+  return IB_OK;
+}
+
+int ib_set_fixed(ib_ctx *c, const uint8_t *mask) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  free_graph(c);
+  CK(cudaStreamSynchronize(c->stream));
+  dfree(c->fixed);
+  c->fixed = nullptr;
+  if (mask && c->np > 0) {
+    CK(dalloc(&c->fixed, (size_t)c->np));
+    CK(copy_sync(c->fixed, mask, (size_t)c->np, c->stream));
+  }
   return IB_OK;
 }
 
@@ -637,7 +662,7 @@ int ib_debug_interp(ib_ctx *c, const double *u, double *U_out) {
   CK(t.get(&U, (size_t)c->np * 3));
   CK(copy_sync(ud, u, 3 * V * sizeof(double), c->stream));
   CK(ensure_binned(c, c->stream));
-  CK(launch_interp(c->g, ud, c->X, c->np, U, nullptr, nullptr, 0, struct_dev(c).perm, c->stream));
+  CK(launch_interp(c->g, ud, c->X, c->np, U, nullptr, nullptr, 0, struct_dev(c).perm, nullptr, c->stream));
   CK(copy_sync(U_out, U, (size_t)c->np * 3 * sizeof(double), c->stream));
   return IB_OK;
 }

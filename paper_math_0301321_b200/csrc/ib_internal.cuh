@@ -21,7 +21,7 @@ struct StructDev {
   const double *stiff;
   int64_t nd;                 // drive
   const int64_t *drive_idx;
-  const double *drive_dir;
+  const double *drive_dir;    // [nd][3], or null: surface-normal drive (normal of the patch)
   double drive_amp;
   int32_t drive_period;
 };
@@ -96,7 +96,8 @@ struct ib_ctx {
   std::vector<ib_patch> patches_h;
   int64_t nd = 0;
   int64_t *drive_idx = nullptr;
-  double *drive_dir = nullptr;
+  double *drive_dir = nullptr;  // null with nd > 0: surface-normal drive
+  uint8_t *fixed = nullptr;     // [np] 1 = point never moves (window plates), or null
   double drive_amp = 0.0;
   int32_t drive_period = 1;
   // control
@@ -158,9 +159,10 @@ cudaError_t launch_force(const StructDev &sd, const long long *dev_n, long long 
 cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g,
                                 const double *f_in, const long long *dev_n, long long n,
                                 double *F, unsigned *rowflag, cudaStream_t s);
+// fixed (may be null): points with fixed[i] != 0 are not moved
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
-                          const int *perm, cudaStream_t s);
+                          const int *perm, const uint8_t *fixed, cudaStream_t s);
 // cell binning: perm = point indices grouped by base cell (5 launches + 1 memset)
 cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
                        unsigned *bsum, int *perm, cudaStream_t s);

@@ -102,6 +102,44 @@ __device__ __forceinline__ void point_force(const StructDev &sd, const ib_patch 
   }
 }
 
+// Direction of driven point d (global index i): the given unit vector, or (drive_dir null)
+// the unit normal of i's patch at the current positions — the window drive "orthogonal to
+// the surface of the window" (PAPER.md 988-993): tangents by central differences along i1
+// and i2 (one-sided at an open edge, periodic with the WRAP flags), n = t1 x t2 / |t1 x t2|.
+__device__ __forceinline__ void drive_direction(const StructDev &sd, int64_t d, int64_t i,
+                                                double dir[3]) {
+  if (sd.drive_dir) {
+    dir[0] = sd.drive_dir[3 * d]; dir[1] = sd.drive_dir[3 * d + 1]; dir[2] = sd.drive_dir[3 * d + 2];
+    return;
+  }
+  int lo = 0, hi = sd.npatch - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (sd.patches[mid].first <= i) lo = mid; else hi = mid - 1;
+  }
+  const ib_patch P = sd.patches[lo];
+  const int64_t li = i - P.first;
+  const int i1 = (int)(li % P.n1), i2 = (int)(li / P.n1);
+  double t[2][3];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const int n = a == 0 ? P.n1 : P.n2, c = a == 0 ? i1 : i2;
+    const bool wrap = (P.flags & (a == 0 ? IB_WRAP1 : IB_WRAP2)) != 0;
+    int cp = c + 1, cm = c - 1;
+    if (wrap) { cp %= n; cm = (cm + n) % n; }
+    else { cp = cp > n - 1 ? n - 1 : cp; cm = cm < 0 ? 0 : cm; }
+    const int64_t jp = P.first + (a == 0 ? (int64_t)i2 * P.n1 + cp : (int64_t)cp * P.n1 + i1);
+    const int64_t jm = P.first + (a == 0 ? (int64_t)i2 * P.n1 + cm : (int64_t)cm * P.n1 + i1);
+#pragma unroll
+    for (int k = 0; k < 3; ++k) t[a][k] = sd.X[3 * jp + k] - sd.X[3 * jm + k];
+  }
+  const double cx = t[0][1] * t[1][2] - t[0][2] * t[1][1];
+  const double cy = t[0][2] * t[1][0] - t[0][0] * t[1][2];
+  const double cz = t[0][0] * t[1][1] - t[0][1] * t[1][0];
+  const double len = sqrt((cx * cx + cy * cy) + cz * cz);
+  dir[0] = cx / len; dir[1] = cy / len; dir[2] = cz / len;
+}
+
 __device__ __forceinline__ double drive_factor(const StructDev &sd, long long n) {
   const long long T = sd.drive_period;
   return sd.drive_amp * sinpi(2.0 * (double)(n % T) / (double)T);
@@ -122,7 +160,9 @@ __global__ void k_drive_add(StructDev sd, const long long *dev_n, long long n, d
   if (d >= sd.nd) return;
   const double a = drive_factor(sd, dev_n ? *dev_n : n);
   const int64_t i = sd.drive_idx[d];
-  for (int c = 0; c < 3; ++c) f_out[3 * i + c] += a * sd.drive_dir[3 * d + c];
+  double dir[3];
+  drive_direction(sd, d, i, dir);
+  for (int c = 0; c < 3; ++c) f_out[3 * i + c] += a * dir[c];
 }
 
 // Spread of the drive forces (few points): one warp per driven point, each lane owning 2 of
@@ -142,13 +182,15 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
   const int jy = axis_weights(sd.X[3 * i + 1], g.invh, wy);
   const int jz = axis_weights(sd.X[3 * i + 2], g.invh, wz);
   const int e = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
+  double dir[3];
+  drive_direction(sd, d, i, dir);
   const size_t x = (jx + e) & (N1 - 1), y = (jy + b) & (N2 - 1);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
     const size_t z = (jz + c0 + 2 * h) & (N3 - 1);
     const size_t cell = (z * N2 + y) * N1 + x;
     const double w = a * wx[e] * wy[b] * wz[c0 + 2 * h];
-    for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], w * sd.drive_dir[3 * d + k]);
+    for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], w * dir[k]);
     if (rowflag && e == 0) rowflag[z * N2 + y] = 1u;
   }
 }
@@ -332,7 +374,8 @@ constexpr int INTERP_THREADS = 128, BOXES = 4, BOXLD = 3 * 64 + 2;   // +2: bank
 
 __global__ void __launch_bounds__(INTERP_THREADS)
 k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
-         long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm) {
+         long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm,
+         const uint8_t *__restrict__ fixed) {
   __shared__ double box[INTERP_THREADS / 32][BOXES][BOXLD];
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -393,7 +436,7 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
   if (live) {
     if (U_out) {
       U_out[3 * i + 0] = U0; U_out[3 * i + 1] = U1; U_out[3 * i + 2] = U2;
-    } else {
+    } else if (!(fixed && fixed[i])) {    // fixed points never move (PAPER.md 919-920)
       const double y0 = x0 + g.dt * U0, y1 = x1 + g.dt * U1, y2 = x2 + g.dt * U2;
       X[3 * i + 0] = y0; X[3 * i + 1] = y1; X[3 * i + 2] = y2;
       bad = !(isfinite(y0) && isfinite(y1) && isfinite(y2));
@@ -407,10 +450,10 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
 
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
-                          const int *perm, cudaStream_t s) {
+                          const int *perm, const uint8_t *fixed, cudaStream_t s) {
   if (np > 0)
     k_interp<<<(unsigned)((np + INTERP_THREADS - 1) / INTERP_THREADS), INTERP_THREADS, 0, s>>>(
-        g, u, X, np, U_out, flag, dev_n, n, perm);
+        g, u, X, np, U_out, flag, dev_n, n, perm, fixed);
   return cudaGetLastError();
 }
 

@@ -20,7 +20,7 @@ IB_WRAP1, IB_WRAP2, IB_STRETCH1, IB_STRETCH2, IB_BEND1, IB_BEND2, IB_TETHER = 1,
 IB_OPT_PRESSURE, IB_OPT_STAGE_TIMING, IB_OPT_GRAPH = 1, 2, 3
 
 EXPORTS = ("ib_create", "ib_create3", "ib_destroy", "ib_set_stream", "ib_set_option", "ib_set_structure",
-           "ib_set_positions", "ib_set_velocity", "ib_set_drive", "ib_step", "ib_get_fields",
+           "ib_set_positions", "ib_set_velocity", "ib_set_drive", "ib_set_fixed", "ib_step", "ib_get_fields",
            "ib_get_positions", "ib_get_step", "ib_set_step", "ib_num_points", "ib_stage_times",
            "ib_launch_count", "ib_last_error", "ib_debug_force", "ib_debug_spread",
            "ib_debug_interp", "ib_debug_rhs", "ib_debug_fluid", "ib_debug_fft")
@@ -66,6 +66,7 @@ def load(path: Optional[str] = None):
     L.ib_set_positions.argtypes = [p, p]
     L.ib_set_velocity.argtypes = [p, p]
     L.ib_set_drive.argtypes = [p, p, i64, p, d, i32]
+    L.ib_set_fixed.argtypes = [p, p]
     L.ib_step.argtypes = [p, i32]
     L.ib_get_fields.argtypes = [p, p, p]
     L.ib_get_positions.argtypes = [p, p]
@@ -110,7 +111,7 @@ def _ptr(a, dtype=np.float64, size: Optional[int] = None, writable=False):
         ptr = a.ctypes.data
     else:   # torch.Tensor
         import torch
-        tdt = {np.float64: torch.float64, np.int64: torch.int64}[dtype]
+        tdt = {np.float64: torch.float64, np.int64: torch.int64, np.uint8: torch.uint8}[dtype]
         if a.dtype != tdt or not a.is_contiguous():
             raise TypeError(f"need a contiguous {tdt} tensor")
         n = a.numel()
@@ -179,10 +180,17 @@ def ib_set_velocity(ctx, u, N) -> None:
 
 
 def ib_set_drive(ctx, idx, direction, amp_per_point: float, period_steps: int) -> None:
+    """direction None: surface-normal drive (the unit normal of each point's patch at X^n)."""
     n = 0 if idx is None else (idx.size if isinstance(idx, np.ndarray) else idx.numel())
     _check(load().ib_set_drive(ctx, _ptr(idx, np.int64) if n else None, n,
-                               _ptr(direction, size=3 * n) if n else None,
+                               _ptr(direction, size=3 * n) if (n and direction is not None) else None,
                                float(amp_per_point), int(period_steps)))
+
+
+def ib_set_fixed(ctx, mask) -> None:
+    """mask: uint8 [np] (1 = the point never moves) or None to clear."""
+    _check(load().ib_set_fixed(ctx, None if mask is None else _ptr(mask, np.uint8,
+                                                                    size=int(load().ib_num_points(ctx)))))
 
 
 def ib_step(ctx, nsteps: int) -> None:
@@ -255,6 +263,8 @@ class IBContext:
             o.set_velocity(cfg.u0)
         if cfg.drive_idx is not None:
             o.set_drive(cfg.drive_idx, cfg.drive_dir, cfg.drive_amp, cfg.drive_period)
+        if getattr(cfg, "fixed", None) is not None:
+            o.set_fixed(cfg.fixed)
         return o
 
     def close(self):
@@ -289,7 +299,11 @@ class IBContext:
 
     def set_drive(self, idx, direction, amp, period):
         ib_set_drive(self.ctx, np.ascontiguousarray(idx, dtype=np.int64),
-                     np.ascontiguousarray(direction, dtype=np.float64), amp, period)
+                     None if direction is None else np.ascontiguousarray(direction, dtype=np.float64),
+                     amp, period)
+
+    def set_fixed(self, mask):
+        ib_set_fixed(self.ctx, None if mask is None else np.ascontiguousarray(mask, dtype=np.uint8))
 
     def set_option(self, opt, value):
         ib_set_option(self.ctx, opt, value)

@@ -361,3 +361,33 @@ def test_step_parity_anisotropic_with_pressure_every_step(ibm, olib, shape):
 def test_halfcube_step_parity(ibm, olib):
     """The 256 x 256 x 128 half-cube workload (gen make_config("4h")): 1 + 9 steps."""
     print(_parity(ibm, olib, make_config("4h")))
+
+
+# ---------------------------------------------------------------- window plates (SURVEY 8(f) row 2)
+@pytest.mark.parametrize("N", [32, (32, 64, 16)])
+def test_window_plate_parity(ibm, olib, N):
+    """Fixed rim points (never move, bitwise) + surface-normal sinusoidal drive on the free
+    disc (PAPER.md 914-922, 988-993) against the oracle after 1 and 10 steps."""
+    from gen import window_config
+    cfg = window_config(N=N, m=24, seed=7, u_amp=0.05)
+    rep = _parity(ibm, olib, cfg, steps=(1, 9), tol=(1e-11, 1e-9))
+    print(rep)
+    with ibm.IBContext.from_config(cfg) as c:
+        c.step(10)
+        X = c.get_positions()
+        f = c.debug_force()
+    fixed = cfg.fixed.astype(bool)
+    assert np.array_equal(X[fixed], cfg.X[fixed])
+    ref = olib.force(X, cfg.patches, cfg.stiffness, 10, cfg.drive_idx, None, cfg.drive_amp,
+                     cfg.drive_period)
+    assert rel_l2(f, ref) < 1e-13
+
+
+def test_normal_drive_rejects_a_line_patch(ibm):
+    from gen import Patch, STRETCH1
+    X = np.array([[0.5, 0.5, 0.5], [0.52, 0.5, 0.5], [0.54, 0.5, 0.5]])
+    with ibm.IBContext(16, 1 / 16, 1, 0.01, 1e-3) as c:
+        c.set_structure(X, [Patch(0, 3, 1, STRETCH1, 0)], np.array([1.0, 1.0, 0.0, 0.02, 0.02, 0.0]))
+        with pytest.raises(ibm.IBError) as e:
+            c.set_drive(np.array([1]), None, 1e-3, 8)
+        assert e.value.code == ibm.IB_EINVAL

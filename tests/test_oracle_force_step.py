@@ -144,3 +144,52 @@ def test_configs_stay_bounded(olib, k, steps, umax, dmax):
     disp = np.max(np.abs(o.get_positions() - cfg.X))
     assert np.isfinite(u).all() and np.max(np.abs(u)) < umax
     assert disp < dmax * cfg.h
+
+
+# ---------------------------------------------------------------- window plates
+def test_window_fixed_points_never_move_and_free_points_do(olib):
+    from gen import window_config
+    cfg = window_config(N=16, m=16, seed=3, u_amp=0.05)
+    o = olib.Oracle.from_config(cfg)
+    X0 = cfg.X.copy()
+    o.step(5)
+    fixed = cfg.fixed.astype(bool)
+    assert fixed.any() and (~fixed).any()
+    assert np.array_equal(o.X[fixed], X0[fixed])                 # bitwise: never updated
+    assert np.min(np.abs(o.X[~fixed] - X0[~fixed]).max(1)) > 0    # every free point moved
+
+
+def test_window_normal_drive_is_orthogonal_to_the_plate(olib):
+    # a flat plate in the plane spanned by e1, e2: every driven force is along e1 x e2 and of
+    # the prescribed magnitude amp * sin(2 pi n / T) (PAPER.md 988-993)
+    from gen import window_config
+    cfg = window_config(N=16, m=12, seed=4, amp=3e-3, period=8)
+    i = np.arange(cfg.X.shape[0])
+    m = 12
+    e1 = cfg.X[1] - cfg.X[0]; e2 = cfg.X[m] - cfg.X[0]
+    flat = cfg.X[0] + (i % m)[:, None] * e1 + (i // m)[:, None] * e2   # undo the bulge
+    step = 2                                                   # sin(2 pi 2/8) = 1
+    f_drive = olib.force(flat, cfg.patches, cfg.stiffness * 0.0, step, cfg.drive_idx, None,
+                         cfg.drive_amp, cfg.drive_period)
+    nrm = np.cross(e1, e2); nrm /= np.linalg.norm(nrm)
+    fd = f_drive[cfg.drive_idx]
+    along = fd @ nrm
+    assert np.allclose(np.abs(along), cfg.drive_amp, rtol=1e-13, atol=0)
+    assert np.max(np.linalg.norm(fd - along[:, None] * nrm, axis=1)) < 1e-15 * cfg.drive_amp * 10
+    assert np.all(f_drive[cfg.fixed.astype(bool)] == 0.0)      # no drive on the bony rim
+    f0 = olib.force(flat, cfg.patches, cfg.stiffness * 0.0, 0, cfg.drive_idx, None,
+                    cfg.drive_amp, cfg.drive_period)
+    assert np.max(np.abs(f0)) == 0.0                            # t = 0 -> sin 0 = 0
+
+
+def test_window_fixed_points_still_spread_their_force(olib):
+    # total spread force equals the total nodal force including the fixed rim's reactions
+    from gen import window_config
+    cfg = window_config(N=16, m=16, seed=5)
+    f = olib.force(cfg.X, cfg.patches, cfg.stiffness, 2, cfg.drive_idx, None, cfg.drive_amp,
+                   cfg.drive_period)
+    fixed = cfg.fixed.astype(bool)
+    assert np.abs(f[fixed]).max() > 0                          # the rim pulls back on the disc
+    F = olib.spread(16, cfg.h, cfg.X, f)
+    assert np.allclose(F.reshape(3, -1).sum(1) * cfg.h ** 3, f.sum(0), rtol=0,
+                       atol=1e-13 * np.abs(f).sum())
