@@ -391,3 +391,19 @@ def test_normal_drive_rejects_a_line_patch(ibm):
         with pytest.raises(ibm.IBError) as e:
             c.set_drive(np.array([1]), None, 1e-3, 8)
         assert e.value.code == ibm.IB_EINVAL
+
+
+# ---------------------------------------------------------------- experiments
+def test_linearity_experiment_on_the_strip(ibm):
+    """PAPER.md 1080-1085: in the linear regime a 10x drive gives 10x the membrane response.
+    cfg3's strip driven with total amplitude 1e-7 vs 1e-6 for 200 steps: the centre-line
+    envelopes agree with the scale to 1 % wherever the base envelope exceeds 1 % of its peak."""
+    from paper_math_0301321_b200 import experiments as ex
+    base = make_config(3)
+    base.drive_amp = 1e-7 / base.drive_idx.size
+    s, ea, _ = ex.run_replica(ex._scaled(base, 1.0), 200, 10)
+    _, eb, _ = ex.run_replica(ex._scaled(base, 10.0), 200, 10)
+    rep = ex.linearity(ea, eb, 10.0)
+    print(rep, ea.max())
+    assert ea.max() > 0 and rep["stations"] > 10
+    assert rep["max_dev"] <= 0.01
