@@ -1,4 +1,4 @@
-// xpass_tma.cu — the inverse x pass of step 3 for N in [64, 256], persistent and TMA-fed:
+// xpass_tma.cu — the inverse x pass of step 3 for N1 in [64, 512], persistent and TMA-fed:
 //
 //   k_xinv_tma : complex-to-real FFT along x of the S1 spectrum -> u^{n+1} (PAPER.md
 //                692-695), with the non-finite check of ib_step.
@@ -36,6 +36,10 @@ struct XT {
   static constexpr size_t XI = (size_t)3 * RB * N * 8 + 3 * NQ * 16; // xinv S1 rows + Nyquist
   static constexpr size_t SI = ((XI > PENC ? XI : PENC) + 1023) & ~(size_t)1023;
   static constexpr int SI_STAGES = 6;
+  // a TMA box is at most 256 doubles wide: rows of N = 512 doubles arrive as HALVES boxes of
+  // HC complex each, stored [comp][half][row][HC]
+  static constexpr int BOXC = N < 256 ? N : 256;        // doubles per box row
+  static constexpr int HALVES = N / BOXC, HC = BOXC / 2;
   static_assert(NTG % 32 == 0, "whole warps per group");
 };
 
@@ -80,7 +84,9 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
         mbar_expect_tx(&full[s], (uint32_t)(3 * RB * (M + 1) * 16));
         for (int c = 0; c < 3; ++c) {
           const int r0 = (c * N3 + z) * N2 + y0;
-          tma_load_2d(b + (size_t)c * RB * M, &map_main, 0, r0, &full[s]);
+          for (int hf = 0; hf < K::HALVES; ++hf)
+            tma_load_2d(b + ((size_t)c * K::HALVES + hf) * RB * K::HC, &map_main, hf * K::BOXC, r0,
+                        &full[s]);
           tma_load_2d(b + (size_t)3 * RB * M + c * K::NQ, &map_nyq, 2 * M, r0, &full[s]);
         }
       }
@@ -97,12 +103,16 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
     const int s = i % S;
     const int z = tile >> lgy, y0 = (tile & (NYB - 1)) * RB;
     double2 *sm = stage0 + (size_t)s * SW;
-    const double2 *in = sm + (size_t)(comp * RB + row) * M;
+    // X_e of this row: half e / HC, position e % HC (one half when N <= 256)
+    const double2 *in = sm + (size_t)comp * RB * M + (size_t)row * K::HC;
+    auto X_at = [&](int e) -> double2 {
+      return in[(e / K::HC) * RB * K::HC + (e % K::HC)];
+    };
     mbar_wait(&full[s], (i / S) & 1);
     const double2 nyq = sm[(size_t)3 * RB * M + comp * K::NQ + row];
     double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * N2 + (y0 + row)) * N);
     auto ld = [&](int e) -> double2 {
-      double2 Xk = in[e], Xm = e == 0 ? nyq : in[M - e];
+      double2 Xk = X_at(e), Xm = e == 0 ? nyq : X_at(M - e);
       if (e == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real
       const double2 A = make_double2(Xk.x + Xm.x, Xk.y - Xm.y);
       const double2 B = make_double2(Xk.x - Xm.x, Xk.y + Xm.y);
@@ -156,17 +166,19 @@ static int xt_rb(int N) {
     case 64: return XT<64>::RB;
     case 128: return XT<128>::RB;
     case 256: return XT<256>::RB;
+    case 512: return XT<512>::RB;
     default: return 0;
   }
 }
 
-bool xpass_supported(int N) { return N >= 64 && N <= 256; }   // N = N1
+bool xpass_supported(int N) { return N >= 64 && N <= 512; }   // N = N1
 
 bool xpass_encode_s1(const FluidGeom &g, const double2 *spec, XMapsS *m) {
   const int N = g.N1;
   if (!xpass_supported(N) || g.N2 % xt_rb(N)) return false;
   const uint64_t rows = (uint64_t)3 * g.N2 * g.N3;
-  return encode_rows(&m->main, spec, rows, 2 * (g.M + 1), (uint64_t)g.P * 16, N, xt_rb(N)) &&
+  const uint32_t boxc = N < 256 ? N : 256;
+  return encode_rows(&m->main, spec, rows, 2 * (g.M + 1), (uint64_t)g.P * 16, boxc, xt_rb(N)) &&
          encode_rows(&m->nyq, spec, rows, 2 * (g.M + 1), (uint64_t)g.P * 16, 2, xt_rb(N));
 }
 
@@ -205,6 +217,7 @@ cudaError_t launch_xinv_tma(const FluidGeom &g, const XMapsS &m, double *out,
     case 64: return xinv_n<64>(g, m, out, twN, twM, flag, dev_n, n, s);
     case 128: return xinv_n<128>(g, m, out, twN, twM, flag, dev_n, n, s);
     case 256: return xinv_n<256>(g, m, out, twN, twM, flag, dev_n, n, s);
+    case 512: return xinv_n<512>(g, m, out, twN, twM, flag, dev_n, n, s);
     default: return cudaErrorInvalidValue;
   }
 }
