@@ -145,6 +145,11 @@ int ib_debug_rhs(ib_ctx *ctx, const double *u, const double *F, double *r_out);
 /* u^{n+1}, p^{n+1} from (u^n, F^n): the fluid part of the step (p_out may be NULL). */
 int ib_debug_fluid(ib_ctx *ctx, const double *u, const double *F, double *u_out,
                    double *p_out);
+/* S3c alone: u^ = (r^ - s (s.r^)/|s|^2)/d and p^ = -i (s.r^)/|s|^2 per mode
+ * (null modes: u^ = r^/d, p^ = 0) from r^; half spectra as interleaved complex,
+ * rhat/uhat [3][N3][N2][N1/2+1], phat [N3][N2][N1/2+1] (may be NULL).  Runs the product z
+ * kernel between an inverse and a forward z transform.  IB_ESTATE unless N3 in [64, 512]. */
+int ib_debug_project(ib_ctx *ctx, const double *rhat, double *uhat, double *phat);
 /* Forward 3-D real-to-complex DFT of a real field [V] (unnormalised, e^{-2 pi i sum k_a j_a/N_a}):
  * out = complex half spectrum [N3][N2][N1/2+1] as interleaved (re, im). */
 int ib_debug_fft(ib_ctx *ctx, const double *in, double *out);

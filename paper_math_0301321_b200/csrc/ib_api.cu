@@ -705,6 +705,55 @@ int ib_debug_fluid(ib_ctx *c, const double *u, const double *F, double *u_out, d
   return IB_OK;
 }
 
+namespace {
+__global__ void k_scale(double *a, size_t n, double f) {
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    a[i] *= f;
+}
+}  // namespace
+
+// S3c alone: u^, p^ from r^ (half spectra [3][N3][N2][N1/2+1] / [N3][N2][N1/2+1], complex
+// interleaved).  Runs the product z kernel (forward z, per-mode solve, inverse z) between an
+// inverse and a forward z transform, so the solve sees r^ (times N3); the scale factors of the
+// unnormalised transforms and of the solve's folded 1/V are undone.  Needs the TMA z pass
+// (N3 in [64, 512]).
+int ib_debug_project(ib_ctx *c, const double *rhat, double *uhat, double *phat) {
+  if (!c || !rhat || !uhat) return fail(IB_EINVAL, "NULL argument");
+  if (!c->maps.z_ok) return fail(IB_ESTATE, "ib_debug_project needs N3 in [64, 512]");
+  const FluidGeom &g = c->g;
+  cudaStream_t s = c->stream;
+  const size_t H = (size_t)(g.M + 1), row = H * 2 * sizeof(double);
+  Tmp t; double2 *ps;
+  CK(t.get(&ps, pspec_elems(c)));
+  for (int comp = 0; comp < 3; ++comp)      // [comp][kz][ky][kx] -> S2 [comp][ky][kz][kx]
+    for (int ky = 0; ky < g.N2; ++ky)
+      CK(cudaMemcpy2DAsync(c->spec2 + ((size_t)comp * g.N2 + ky) * g.N3 * g.P, (size_t)g.P * sizeof(double2),
+                           rhat + (((size_t)comp * g.N3) * g.N2 + ky) * H * 2, (size_t)g.N2 * row,
+                           row, (size_t)g.N3, cudaMemcpyDefault, s));
+  const Sym sy = sym_of(c);
+  CK(launch_colfft(g, 4, c->maps, nullptr, c->tw[2], sy, s));    // inverse z
+  CK(launch_colfft(g, 0, c->maps, ps, c->tw[2], sy, s));         // z, solve, inverse z
+  CK(launch_colfft(g, 3, c->maps, nullptr, c->tw[2], sy, s));    // forward z
+  // unnormalised z transforms around the solve (which folds in 1/V): u^ comes out scaled by
+  // N3^2 / V, p^ (written at solve time, between the z transforms) by N3 / V
+  const double V = (double)g.V, N3 = (double)g.N3;
+  k_scale<<<592, 256, 0, s>>>(reinterpret_cast<double *>(c->spec2), 3 * spec1_elems(c) * 2, V / (N3 * N3));
+  k_scale<<<592, 256, 0, s>>>(reinterpret_cast<double *>(ps), spec1_elems(c) * 2, V / N3);
+  c->launches += 5;
+  for (int comp = 0; comp < 3; ++comp)      // S2 -> [comp][kz][ky][kx]
+    for (int ky = 0; ky < g.N2; ++ky)
+      CK(cudaMemcpy2DAsync(uhat + (((size_t)comp * g.N3) * g.N2 + ky) * H * 2, (size_t)g.N2 * row,
+                           c->spec2 + ((size_t)comp * g.N2 + ky) * g.N3 * g.P, (size_t)g.P * sizeof(double2),
+                           row, (size_t)g.N3, cudaMemcpyDefault, s));
+  if (phat)
+    for (int ky = 0; ky < g.N2; ++ky)
+      CK(cudaMemcpy2DAsync(phat + (size_t)ky * H * 2, (size_t)g.N2 * row,
+                           ps + (size_t)ky * g.N3 * g.P, (size_t)g.P * sizeof(double2),
+                           row, (size_t)g.N3, cudaMemcpyDefault, s));
+  CK(cudaStreamSynchronize(s));
+  return IB_OK;
+}
+
 int ib_debug_fft(ib_ctx *c, const double *in, double *out) {
   if (!c || !in || !out) return fail(IB_EINVAL, "NULL argument");
   Tmp t; double *ind;

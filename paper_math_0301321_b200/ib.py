@@ -23,7 +23,8 @@ EXPORTS = ("ib_create", "ib_create3", "ib_destroy", "ib_set_stream", "ib_set_opt
            "ib_set_positions", "ib_set_velocity", "ib_set_drive", "ib_set_fixed", "ib_step", "ib_get_fields",
            "ib_get_positions", "ib_get_step", "ib_set_step", "ib_num_points", "ib_stage_times",
            "ib_launch_count", "ib_last_error", "ib_debug_force", "ib_debug_spread",
-           "ib_debug_interp", "ib_debug_rhs", "ib_debug_fluid", "ib_debug_fft")
+           "ib_debug_interp", "ib_debug_rhs", "ib_debug_fluid", "ib_debug_project",
+           "ib_debug_fft")
 
 
 class IBError(RuntimeError):
@@ -85,6 +86,7 @@ def load(path: Optional[str] = None):
     L.ib_debug_rhs.argtypes = [p, p, p, p]
     L.ib_debug_fluid.argtypes = [p, p, p, p, p]
     L.ib_debug_fft.argtypes = [p, p, p]
+    L.ib_debug_project.argtypes = [p, p, p, p]
     for name in EXPORTS:
         if name not in ("ib_create", "ib_create3", "ib_destroy", "ib_get_step", "ib_num_points",
                         "ib_launch_count", "ib_last_error"):
@@ -377,6 +379,16 @@ class IBContext:
         _check(load().ib_debug_fluid(self.ctx, _ptr(u, size=3 * self.V), _ptr(F, size=3 * self.V),
                                      _ptr(un), _ptr(p)))
         return un, p
+
+    def debug_project(self, rhat, want_p=True):
+        """S3c on a half spectrum rhat [3][N3][N2][N1/2+1] (complex) -> (uhat, phat)."""
+        n1, n2, n3 = self.dims
+        r = np.ascontiguousarray(np.stack([np.asarray(rhat).real, np.asarray(rhat).imag], -1),
+                                 dtype=np.float64)
+        u = np.empty((3, n3, n2, n1 // 2 + 1, 2))
+        p = np.empty((n3, n2, n1 // 2 + 1, 2)) if want_p else None
+        _check(load().ib_debug_project(self.ctx, _ptr(r, size=r.size), _ptr(u), _ptr(p)))
+        return u[..., 0] + 1j * u[..., 1], (None if p is None else p[..., 0] + 1j * p[..., 1])
 
     def debug_fft(self, x):
         n1, n2, n3 = self.dims

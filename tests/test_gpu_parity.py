@@ -407,3 +407,17 @@ def test_linearity_experiment_on_the_strip(ibm):
     print(rep, ea.max())
     assert ea.max() > 0 and rep["stations"] > 10
     assert rep["max_dev"] <= 0.01
+
+
+@pytest.mark.parametrize("shape", [64, (16, 16, 64), (64, 32, 128)])
+def test_project_alone_matches_oracle_solve(ibm, olib, shape):
+    """S3c in isolation (ib_debug_project): the GPU's per-mode solve of r^ = rfftn(r) against
+    rfftn of the oracle's solve of r (numpy's FFT as a library step)."""
+    n1, n2, n3 = (shape,) * 3 if isinstance(shape, int) else shape
+    r = np.random.default_rng(41).standard_normal((3, n3, n2, n1))
+    h, rho, mu, dt = 1.0 / n1, 1.2, 0.03, 2e-3
+    with ibm.IBContext(shape, h, rho, mu, dt) as c:
+        uh, ph = c.debug_project(np.fft.rfftn(r, axes=(1, 2, 3)))
+    u, p = olib.solve(shape, h, rho, mu, dt, r)
+    assert rel_l2(uh, np.fft.rfftn(u, axes=(1, 2, 3))) < 1e-13
+    assert rel_l2(ph, np.fft.rfftn(p)) < 1e-12
