@@ -28,6 +28,9 @@ enum { MODE_Z = 0, MODE_YFWD = 1, MODE_YINV = 2, MODE_ZFWD = 3, MODE_ZINV = 4 };
 #ifndef IBK_YG256
 #define IBK_YG256 1
 #endif
+#ifndef IBK_ZG128
+#define IBK_ZG128 4
+#endif
 
 // Column tile geometry: C columns (C = 8 -> 128-byte rows, SWIZZLE_128B; C = 4 -> 64-byte
 // rows, SWIZZLE_64B), N rows, NC components (3 when the tile is solved, 1 for the y passes),
@@ -60,7 +63,7 @@ template <int N, int MODE> struct ColCfg {
   static constexpr int G = ZM ? (N == 128 || N == 256 ? 2 : 1) : (N >= 512 ? 1 : (N == 256 ? 1 : 4));
 #else
   static constexpr int NC = ZM ? 3 : 1;
-  static constexpr int G = ZM ? (N == 128 || N == 256 ? 2 : 1) : (N >= 512 ? 1 : (N == 256 ? IBK_YG256 : 4));
+  static constexpr int G = ZM ? (N == 256 ? 2 : (N <= 128 ? IBK_ZG128 : 1)) : (N >= 512 ? 1 : (N == 256 ? IBK_YG256 : 4));
 #endif
   static constexpr size_t SB = (size_t)NC * N * C * 16;
   static constexpr int S0 = (int)((200 * 1024) / SB);
