@@ -153,6 +153,10 @@ int ib_debug_project(ib_ctx *ctx, const double *rhat, double *uhat, double *phat
 /* Forward 3-D real-to-complex DFT of a real field [V] (unnormalised, e^{-2 pi i sum k_a j_a/N_a}):
  * out = complex half spectrum [N3][N2][N1/2+1] as interleaved (re, im). */
 int ib_debug_fft(ib_ctx *ctx, const double *in, double *out);
+/* Unnormalised inverse 3-D DFT (S3d) of a half spectrum [N3][N2][N1/2+1] (interleaved
+ * re, im; the Hermitian half of a real field's spectrum) -> real field [V], through the
+ * product inverse passes.  IB_ESTATE unless N3 in [64, 512]. */
+int ib_debug_ifft(ib_ctx *ctx, const double *in, double *out);
 
 #ifdef __cplusplus
 }

@@ -754,6 +754,34 @@ int ib_debug_project(ib_ctx *c, const double *rhat, double *uhat, double *phat) 
   return IB_OK;
 }
 
+// S3d alone: unnormalised inverse 3-D DFT of a half spectrum in [N3][N2][N1/2+1] (complex
+// interleaved) -> real out [V], through the product inverse passes (z, y, then the x C2R),
+// i.e. sum_k X_k e^{+2 pi i sum k_a j_a / N_a} over the full Hermitian spectrum.  The TMA
+// column passes transform 3 component slots; slot 0 carries the data.
+int ib_debug_ifft(ib_ctx *c, const double *in, double *out) {
+  if (!c || !in || !out) return fail(IB_EINVAL, "NULL argument");
+  const FluidGeom &g = c->g;
+  cudaStream_t s = c->stream;
+  const size_t H = (size_t)(g.M + 1), row = H * 2 * sizeof(double);
+  CK(cudaMemsetAsync(c->spec2, 0, 3 * spec1_elems(c) * sizeof(double2), s));
+  for (int ky = 0; ky < g.N2; ++ky)          // [kz][ky][kx] -> S2 slot 0 [ky][kz][kx]
+    CK(cudaMemcpy2DAsync(c->spec2 + (size_t)ky * g.N3 * g.P, (size_t)g.P * sizeof(double2),
+                         in + (size_t)ky * H * 2, (size_t)g.N2 * row, row, (size_t)g.N3,
+                         cudaMemcpyDefault, s));
+  Tmp t; double *o;
+  CK(t.get(&o, 3 * (size_t)g.V));
+  if (c->maps.z_ok) {
+    CK(launch_colfft(g, 4, c->maps, nullptr, c->tw[2], sym_of(c), s));
+  } else {                                   // inverse z through the pressure path's pass
+    return fail(IB_ESTATE, "ib_debug_ifft needs N3 in [64, 512]");
+  }
+  CK(yinv(c, s));
+  CK(xinv(c, o, nullptr, 0, nullptr, s));
+  c->launches += 3;
+  CK(copy_sync(out, o, (size_t)g.V * sizeof(double), s));
+  return IB_OK;
+}
+
 int ib_debug_fft(ib_ctx *c, const double *in, double *out) {
   if (!c || !in || !out) return fail(IB_EINVAL, "NULL argument");
   Tmp t; double *ind;

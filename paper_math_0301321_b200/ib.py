@@ -24,7 +24,7 @@ EXPORTS = ("ib_create", "ib_create3", "ib_destroy", "ib_set_stream", "ib_set_opt
            "ib_get_positions", "ib_get_step", "ib_set_step", "ib_num_points", "ib_stage_times",
            "ib_launch_count", "ib_last_error", "ib_debug_force", "ib_debug_spread",
            "ib_debug_interp", "ib_debug_rhs", "ib_debug_fluid", "ib_debug_project",
-           "ib_debug_fft")
+           "ib_debug_fft", "ib_debug_ifft")
 
 
 class IBError(RuntimeError):
@@ -87,6 +87,7 @@ def load(path: Optional[str] = None):
     L.ib_debug_fluid.argtypes = [p, p, p, p, p]
     L.ib_debug_fft.argtypes = [p, p, p]
     L.ib_debug_project.argtypes = [p, p, p, p]
+    L.ib_debug_ifft.argtypes = [p, p, p]
     for name in EXPORTS:
         if name not in ("ib_create", "ib_create3", "ib_destroy", "ib_get_step", "ib_num_points",
                         "ib_launch_count", "ib_last_error"):
@@ -389,6 +390,15 @@ class IBContext:
         p = np.empty((n3, n2, n1 // 2 + 1, 2)) if want_p else None
         _check(load().ib_debug_project(self.ctx, _ptr(r, size=r.size), _ptr(u), _ptr(p)))
         return u[..., 0] + 1j * u[..., 1], (None if p is None else p[..., 0] + 1j * p[..., 1])
+
+    def debug_ifft(self, X):
+        """Unnormalised inverse DFT of a half spectrum [N3][N2][N1/2+1] -> real [N3][N2][N1]."""
+        n1, n2, n3 = self.dims
+        xin = np.ascontiguousarray(np.stack([np.asarray(X).real, np.asarray(X).imag], -1),
+                                   dtype=np.float64)
+        out = np.empty((n3, n2, n1))
+        _check(load().ib_debug_ifft(self.ctx, _ptr(xin, size=xin.size), _ptr(out)))
+        return out
 
     def debug_fft(self, x):
         n1, n2, n3 = self.dims

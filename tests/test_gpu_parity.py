@@ -421,3 +421,46 @@ def test_project_alone_matches_oracle_solve(ibm, olib, shape):
     u, p = olib.solve(shape, h, rho, mu, dt, r)
     assert rel_l2(uh, np.fft.rfftn(u, axes=(1, 2, 3))) < 1e-13
     assert rel_l2(ph, np.fft.rfftn(p)) < 1e-12
+
+
+@pytest.mark.parametrize("shape", [64, (32, 64, 128), (256, 64, 64)])
+def test_inverse_fft_alone(ibm, olib, shape):
+    """S3d in isolation (ib_debug_ifft): the product inverse passes on X = rfftn(x) give the
+    unnormalised inverse V x; cross-checked against the oracle's radix-2 FFT on the full
+    Hermitian spectrum."""
+    n1, n2, n3 = (shape,) * 3 if isinstance(shape, int) else shape
+    x = np.random.default_rng(43).standard_normal((n3, n2, n1))
+    X = np.fft.rfftn(x)
+    with ibm.IBContext(shape, 1.0 / n1, 1.0, 0.01, 1e-3) as c:
+        got = c.debug_ifft(X)
+    V = n1 * n2 * n3
+    assert rel_l2(got, V * x) < 1e-14 * np.log2(V)
+    if V <= 64 ** 3:
+        full = np.fft.fftn(x)
+        assert rel_l2(got, olib.fft3(full, +1).real) < 1e-14 * np.log2(V)
+
+
+def test_checkpoint_resume_matches_straight_run(ibm):
+    """the state is (u, X, n); saving it with ib_get_fields/positions/step and
+    restoring it in a fresh context with ib_set_velocity/structure/step resumes the run (to
+    the fp64 atomic-order tolerance, not bitwise)."""
+    cfg = small_sheet_config(N=32, n1=20, n2=14, seed=44, u_amp=0.2)
+    with ibm.IBContext.from_config(cfg) as a:
+        a.step(10)
+        u_ref, _ = a.get_fields()
+        X_ref = a.get_positions()
+    with ibm.IBContext.from_config(cfg) as b:
+        b.step(4)
+        u4, _ = b.get_fields()
+        X4 = b.get_positions()
+        n4 = b.n
+    with ibm.IBContext.from_config(cfg) as r:       # fresh context, restored state
+        r.set_structure(X4, cfg.patches, cfg.stiffness)
+        r.set_drive(cfg.drive_idx, cfg.drive_dir, cfg.drive_amp, cfg.drive_period)
+        r.set_velocity(u4)
+        r.set_step(n4)
+        r.step(6)
+        assert r.n == 10
+        u, _ = r.get_fields()
+        X = r.get_positions()
+    assert rel_l2(u, u_ref) < 1e-12 and rel_l2(X - cfg.X, X_ref - cfg.X) < 1e-10
