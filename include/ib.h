@@ -81,7 +81,7 @@ ib_ctx *ib_create(int32_t N, double h, double rho, double mu, double dt);
  * [0, N1 h) x [0, N2 h) x [0, N3 h) — e.g. the paper's 256 x 256 x 128 half-cube model
  * (PAPER.md 1003-1007).  Fields are then [3][N3][N2][N1] (x fastest), p is [N3][N2][N1].
  * Rejects, besides the ib_create cases per axis: N2 not a multiple of the x-pass row
- * block (64 / max(1, N1/32), at most N1: 8 for N1 = 256, 4 for 512). */
+ * block (32 / max(1, N1/32), at most N1: 4 for N1 = 256, 2 for 512). */
 ib_ctx *ib_create3(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu,
                    double dt);
 void ib_destroy(ib_ctx *ctx);

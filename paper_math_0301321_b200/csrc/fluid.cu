@@ -21,10 +21,13 @@
 namespace ibk {
 
 // ------------------------------------------------------------------ tile configuration
+#ifndef IBK_XRB
+#define IBK_XRB 32   // rows x threads-per-pencil: RB = 4 rows at N1 = 256 (5 CTAs per SM)
+#endif
 template <int N> struct XCfg {      // x passes: RB rows of one z-plane per CTA
   static constexpr int M = N / 2;
   static constexpr int T = Plan<M>::T;
-  static constexpr int RB = (64 / T) < N ? (64 / T) : N;
+  static constexpr int RB = (IBK_XRB / T) < N ? (IBK_XRB / T) : N;
 };
 #ifndef IBK_YC
 #define IBK_YC 8

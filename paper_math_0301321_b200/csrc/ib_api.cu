@@ -237,7 +237,7 @@ static bool pow2_in(int32_t n, int32_t lo, int32_t hi) { return n >= lo && n <= 
 // rows per x-pass tile for a row length N1 (= XCfg<N1>::RB): the y extent N2 must be a
 // multiple of it
 static int32_t x_rows(int32_t N1) {
-  const int32_t M = N1 / 2, T = M >= 16 ? M / 16 : 1, rb = 64 / T;
+  const int32_t M = N1 / 2, T = M >= 16 ? M / 16 : 1, rb = 32 / T;
   return rb < N1 ? rb : N1;
 }
 
