@@ -209,7 +209,10 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
 }
 
 // ------------------------------------------------------------------ force + spread
-constexpr int SPREAD_THREADS = 256;
+#ifndef IBK_SPT
+#define IBK_SPT 256
+#endif
+constexpr int SPREAD_THREADS = IBK_SPT;
 constexpr int REC = 17;    // 12 weights + 3 forces, padded to an odd stride (bank spread)
 constexpr int PTAB = 64;   // patch table entries staged in shared memory
 
@@ -226,82 +229,68 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
   if (lane < REC) rec[warp][32][lane] = 0.0;
   __syncthreads();
   const ib_patch *pt = small ? ptab : sd.patches;
-  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
   const size_t V = (size_t)g.V;
-  double *r = rec[warp][lane];
-  unsigned key = 0xffffffffu;
-  bool live = false;
-  if (k < sd.np) {
-#ifdef IBK_SP_NOPERM   // dev timing experiment only
-    const int64_t i = k;
-#else
-    const int64_t i = sd.perm ? (int64_t)__ldg(&sd.perm[k]) : k;   // cell-binned order
-#endif
-    double f[3];
-    if (FROM_ARRAY) {
-      f[0] = __ldg(&f_in[3 * i]); f[1] = __ldg(&f_in[3 * i + 1]); f[2] = __ldg(&f_in[3 * i + 2]);
-    } else {
-#ifdef IBK_SP_NOFORCE   // dev timing experiment only
-      f[0] = 1e-3 * (double)(i & 7); f[1] = 1e-3; f[2] = -1e-3;
-#else
-      point_force(sd, pt, i, f);
-#endif
-    }
-    const double ih3 = g.invh * g.invh * g.invh;
-    live = (f[0] != 0.0) || (f[1] != 0.0) || (f[2] != 0.0);
-    const int jx = axis_weights(__ldg(&sd.X[3 * i + 0]), g.invh, r + 0) & (N1 - 1);
-    const int jy = axis_weights(__ldg(&sd.X[3 * i + 1]), g.invh, r + 4) & (N2 - 1);
-    const int jz = axis_weights(__ldg(&sd.X[3 * i + 2]), g.invh, r + 8) & (N3 - 1);
-    r[12] = f[0] * ih3; r[13] = f[1] * ih3; r[14] = f[2] * ih3;
-    key = ((unsigned)jz * N2 + (unsigned)jy) * N1 + (unsigned)jx;
-  }
-  __syncwarp();
   const int lg1 = __ffs(N1) - 1, lg2 = __ffs(N2) - 1;   // powers of two: no division below
-  unsigned todo = __ballot_sync(0xffffffffu, live);
-#ifdef IBK_SP_NOGROUPS   // dev timing experiment only
-  if (live && r[12] == 1.2345e300) F[0] = 1.0;
-  todo = 0;
-#endif
+  const double ih3 = g.invh * g.invh * g.invh;
+  double *r = rec[warp][lane];
   // lane -> outputs (a, b, c0 | c0 + 2, component 0..2)
   const int a = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
-  while (todo) {
-    const int leader = __ffs(todo) - 1;
-    const unsigned kl = __shfl_sync(0xffffffffu, key, leader);
-    const unsigned grp = __ballot_sync(0xffffffffu, key == kl) & todo;
-    todo &= ~grp;
-    double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
-    unsigned m = grp;
-#ifdef IBK_SP_NOLOOP   // dev timing experiment only
-    m = 0;
-#endif
-    while (m) {              // two members per iteration (record 32 = zero pads the tail)
-      const int p = __ffs(m) - 1;
-      m &= m - 1;
-      const int p2 = m ? __ffs(m) - 1 : 32;
-      m &= m - 1;
-      const double *q = rec[warp][p], *q2 = rec[warp][p2];
-      const double wab = q[a] * q[4 + b], wab2 = q2[a] * q2[4 + b];
-      const double w0 = wab * q[8 + c0], w1 = wab * q[10 + c0];
-      const double v0 = wab2 * q2[8 + c0], v1 = wab2 * q2[10 + c0];
-      acc[0] += q[12] * w0 + q2[12] * v0; acc[1] += q[12] * w1 + q2[12] * v1;
-      acc[2] += q[13] * w0 + q2[13] * v0; acc[3] += q[13] * w1 + q2[13] * v1;
-      acc[4] += q[14] * w0 + q2[14] * v0; acc[5] += q[14] * w1 + q2[14] * v1;
+  // persistent: the grid walks the points in blocks of SPREAD_THREADS
+  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x; k0 < sd.np; k0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t k = k0 + threadIdx.x;
+    unsigned key = 0xffffffffu;
+    bool live = false;
+    if (k < sd.np) {
+      const int64_t i = sd.perm ? (int64_t)__ldg(&sd.perm[k]) : k;   // cell-binned order
+      double f[3];
+      if (FROM_ARRAY) {
+        f[0] = __ldg(&f_in[3 * i]); f[1] = __ldg(&f_in[3 * i + 1]); f[2] = __ldg(&f_in[3 * i + 2]);
+      } else {
+        point_force(sd, pt, i, f);
+      }
+      live = (f[0] != 0.0) || (f[1] != 0.0) || (f[2] != 0.0);
+      const int jx = axis_weights(__ldg(&sd.X[3 * i + 0]), g.invh, r + 0) & (N1 - 1);
+      const int jy = axis_weights(__ldg(&sd.X[3 * i + 1]), g.invh, r + 4) & (N2 - 1);
+      const int jz = axis_weights(__ldg(&sd.X[3 * i + 2]), g.invh, r + 8) & (N3 - 1);
+      r[12] = f[0] * ih3; r[13] = f[1] * ih3; r[14] = f[2] * ih3;
+      key = ((unsigned)jz * N2 + (unsigned)jy) * N1 + (unsigned)jx;
     }
-    const unsigned jx = kl & (N1 - 1), jy = (kl >> lg1) & (N2 - 1), jz = kl >> (lg1 + lg2);
-    const size_t x = (jx + a) & (N1 - 1), y = (jy + b) & (N2 - 1);
-    const size_t z0 = (jz + c0) & (N3 - 1), z1 = (jz + c0 + 2) & (N3 - 1);
-    const size_t e0 = (z0 * N2 + y) * N1 + x, e1 = (z1 * N2 + y) * N1 + x;
-#ifdef IBK_SP_NOFLUSH   // dev timing experiment only
-    if (acc[0] == 1.2345e300)
-#endif
-    atomicAdd(&F[e0], acc[0]);          atomicAdd(&F[e1], acc[1]);
-    atomicAdd(&F[V + e0], acc[2]);      atomicAdd(&F[V + e1], acc[3]);
-    atomicAdd(&F[2 * V + e0], acc[4]);  atomicAdd(&F[2 * V + e1], acc[5]);
-    if (rowflag && a == 0) {                    // mark rows (y, z0), (y, z1) of F non-zero
-      rowflag[z0 * N2 + y] = 1u;
-      rowflag[z1 * N2 + y] = 1u;
+    __syncwarp();
+    unsigned todo = __ballot_sync(0xffffffffu, live);
+    while (todo) {
+      const int leader = __ffs(todo) - 1;
+      const unsigned kl = __shfl_sync(0xffffffffu, key, leader);
+      const unsigned grp = __ballot_sync(0xffffffffu, key == kl) & todo;
+      todo &= ~grp;
+      double acc[6] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+      unsigned m = grp;
+      while (m) {              // two members per iteration (record 32 = zero pads the tail)
+        const int p = __ffs(m) - 1;
+        m &= m - 1;
+        const int p2 = m ? __ffs(m) - 1 : 32;
+        m &= m - 1;
+        const double *q = rec[warp][p], *q2 = rec[warp][p2];
+        const double wab = q[a] * q[4 + b], wab2 = q2[a] * q2[4 + b];
+        const double w0 = wab * q[8 + c0], w1 = wab * q[10 + c0];
+        const double v0 = wab2 * q2[8 + c0], v1 = wab2 * q2[10 + c0];
+        acc[0] += q[12] * w0 + q2[12] * v0; acc[1] += q[12] * w1 + q2[12] * v1;
+        acc[2] += q[13] * w0 + q2[13] * v0; acc[3] += q[13] * w1 + q2[13] * v1;
+        acc[4] += q[14] * w0 + q2[14] * v0; acc[5] += q[14] * w1 + q2[14] * v1;
+      }
+      const unsigned jx = kl & (N1 - 1), jy = (kl >> lg1) & (N2 - 1), jz = kl >> (lg1 + lg2);
+      const size_t x = (jx + a) & (N1 - 1), y = (jy + b) & (N2 - 1);
+      const size_t z0 = (jz + c0) & (N3 - 1), z1 = (jz + c0 + 2) & (N3 - 1);
+      const size_t e0 = (z0 * N2 + y) * N1 + x, e1 = (z1 * N2 + y) * N1 + x;
+      atomicAdd(&F[e0], acc[0]);          atomicAdd(&F[e1], acc[1]);
+      atomicAdd(&F[V + e0], acc[2]);      atomicAdd(&F[V + e1], acc[3]);
+      atomicAdd(&F[2 * V + e0], acc[4]);  atomicAdd(&F[2 * V + e1], acc[5]);
+      if (rowflag && a == 0) {                  // mark rows (y, z0), (y, z1) of F non-zero
+        rowflag[z0 * N2 + y] = 1u;
+        rowflag[z1 * N2 + y] = 1u;
+      }
     }
+    __syncwarp();                               // records reused by the next block of points
   }
 }
 
@@ -315,8 +304,19 @@ cudaError_t launch_force(const StructDev &sd, const long long *dev_n, long long 
 cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const double *f_in,
                                 const long long *dev_n, long long n, double *F,
                                 unsigned *rowflag, cudaStream_t s) {
-  const unsigned blocks = (unsigned)((sd.np + SPREAD_THREADS - 1) / SPREAD_THREADS);
   if (sd.np > 0) {
+    static int cap[2] = {0, 0};                 // resident blocks on the device (persistent)
+    const int fa = f_in ? 1 : 0;
+    if (!cap[fa]) {
+      int dev = 0, nsm = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+      if (f_in) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_force_spread<true>, SPREAD_THREADS, 0);
+      else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_force_spread<false>, SPREAD_THREADS, 0);
+      cap[fa] = nsm * (per > 0 ? per : 1);
+    }
+    const int64_t need = (sd.np + SPREAD_THREADS - 1) / SPREAD_THREADS;
+    const unsigned blocks = (unsigned)(need < cap[fa] ? need : cap[fa]);
     if (f_in)
       k_force_spread<true><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag);
     else
