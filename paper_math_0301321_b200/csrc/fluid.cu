@@ -93,8 +93,13 @@ cudaError_t init_tables(ib_ctx *c) {
 // shared memory with cp.async; each thread then computes r at the 2*RMAX cells of its
 // first-pass elements (z_e = r_2e + i r_2e+1) from that tile plus the z +- 1 rows (L2),
 // straight into registers.  The tile is then reused as the FFT exchange buffer.
+// 5 CTAs (15 warps) per SM: <= 128 registers, 4 resident warps per scheduler (266 vs 287 us
+// at 256^3 with 4 CTAs; 6 CTAs spill)
+#ifndef IBK_XMINB
+#define IBK_XMINB 5
+#endif
 template <int N, int MODE>
-__global__ void __launch_bounds__(3 * XCfg<N>::RB * XCfg<N>::T)
+__global__ void __launch_bounds__(3 * XCfg<N>::RB * XCfg<N>::T, IBK_XMINB)
 k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
        const double *__restrict__ in, double *r_out, double2 *spec,
        const double2 *__restrict__ twN, const double2 *__restrict__ twM,

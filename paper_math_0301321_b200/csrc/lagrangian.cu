@@ -66,7 +66,7 @@ __device__ __forceinline__ void spring(const double *__restrict__ X, double xi, 
 
 // pt: the patch table (shared-memory copy when it fits, else sd.patches)
 __device__ __forceinline__ void point_force(const StructDev &sd, const ib_patch *pt, int64_t i,
-                                            double f[3]) {
+                                            double f[3], double xyz[3]) {
   int lo = 0, hi = sd.npatch - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -78,10 +78,12 @@ __device__ __forceinline__ void point_force(const StructDev &sd, const ib_patch 
   const uint32_t fl = P->flags;
   const int64_t npts = (int64_t)n1 * n2;
   const int64_t li = i - first;
-  const int i1 = (int)(li % n1), i2 = (int)(li / n1);
+  // 32-bit index arithmetic: a patch holds < 2^31 points (ib_set_structure checks np)
+  const int i2 = (int)((unsigned)li / (unsigned)n1), i1 = (int)li - i2 * n1;
   const double *b = sd.stiff + P->param_off;
   const double xi = __ldg(&sd.X[3 * i + 0]), yi = __ldg(&sd.X[3 * i + 1]),
                zi = __ldg(&sd.X[3 * i + 2]);
+  xyz[0] = xi; xyz[1] = yi; xyz[2] = zi;
   f[0] = f[1] = f[2] = 0.0;
 #pragma unroll
   for (int fam = 0; fam < 4; ++fam) {
@@ -95,13 +97,13 @@ __device__ __forceinline__ void point_force(const StructDev &sd, const ib_patch 
     const bool wrap = (fl & (ax1 ? IB_WRAP1 : IB_WRAP2)) != 0;
     int cf = c + off;
     if (cf < n || wrap) {
-      cf %= n;
+      while (cf >= n) cf -= n;
       const int64_t lj = ax1 ? (int64_t)i2 * n1 + cf : (int64_t)cf * n1 + i1;
       spring(sd.X, xi, yi, zi, first + lj, __ldg(&k[li]), __ldg(&L0[li]), f);
     }
     int cb = c - off;
     if (cb >= 0 || wrap) {
-      cb = (cb % n + n) % n;
+      while (cb < 0) cb += n;
       const int64_t lj = ax1 ? (int64_t)i2 * n1 + cb : (int64_t)cb * n1 + i1;
       spring(sd.X, xi, yi, zi, first + lj, __ldg(&k[lj]), __ldg(&L0[lj]), f);
     }
@@ -161,8 +163,8 @@ __device__ __forceinline__ double drive_factor(const StructDev &sd, long long n)
 __global__ void k_force(StructDev sd, const long long *dev_n, long long n, double *f_out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= sd.np) return;
-  double f[3];
-  point_force(sd, sd.patches, i, f);
+  double f[3], xyz[3];
+  point_force(sd, sd.patches, i, f, xyz);
   f_out[3 * i + 0] = f[0];
   f_out[3 * i + 1] = f[1];
   f_out[3 * i + 2] = f[2];
@@ -210,23 +212,28 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
 
 // ------------------------------------------------------------------ force + spread
 #ifndef IBK_SPT
-#define IBK_SPT 256
+#define IBK_SPT 128
 #endif
 constexpr int SPREAD_THREADS = IBK_SPT;
-constexpr int REC = 17;    // 12 weights + 3 forces, padded to an odd stride (bank spread)
+// per-point record: [0,16) wx[a] wy[b] at b*4+a; [16,22) f*wz[0], f*wz[2]; [22,28) f*wz[1],
+// f*wz[3] (f scaled by 1/h^3); stride 30 doubles = 15 x 16 B (conflict-free 128-bit access)
+constexpr int REC = 30;
 constexpr int PTAB = 64;   // patch table entries staged in shared memory
 
+#ifndef IBK_SP_MINB
+#define IBK_SP_MINB 1
+#endif
 template <bool FROM_ARRAY>
-__global__ void __launch_bounds__(SPREAD_THREADS)
+__global__ void __launch_bounds__(SPREAD_THREADS, IBK_SP_MINB)
 k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, double *F,
                unsigned *rowflag) {
-  __shared__ double rec[SPREAD_THREADS / 32][33][REC];     // record 32: zeros (unroll tail)
+  __shared__ __align__(16) double rec[SPREAD_THREADS / 32][33][REC];   // record 32: zeros (tail)
   __shared__ ib_patch ptab[PTAB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool small = sd.npatch <= PTAB;
   if (!FROM_ARRAY && small)
     for (int q = threadIdx.x; q < sd.npatch; q += blockDim.x) ptab[q] = sd.patches[q];
-  if (lane < REC) rec[warp][32][lane] = 0.0;
+  if (lane < REC) rec[warp][32][lane] = 0.0;   // (REC <= 32)
   __syncthreads();
   const ib_patch *pt = small ? ptab : sd.patches;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
@@ -235,25 +242,44 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
   const double ih3 = g.invh * g.invh * g.invh;
   double *r = rec[warp][lane];
   // lane -> outputs (a, b, c0 | c0 + 2, component 0..2)
-  const int a = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
-  // persistent: the grid walks the points in blocks of SPREAD_THREADS
-  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x; k0 < sd.np; k0 += (int64_t)gridDim.x * blockDim.x) {
+  const int a = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4, ab = lane & 15;
+  // persistent: the grid walks the points in blocks of SPREAD_THREADS; the binned index of
+  // the next block is fetched one iteration ahead (one less dependent load per point)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  auto point_at = [&](int64_t k) -> int64_t {
+    return k < sd.np ? (sd.perm ? (int64_t)__ldg(&sd.perm[k]) : k) : 0;
+  };
+  int64_t inext = point_at((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  for (int64_t k0 = (int64_t)blockIdx.x * blockDim.x; k0 < sd.np; k0 += stride) {
     const int64_t k = k0 + threadIdx.x;
+    const int64_t i = inext;
+    inext = point_at(k + stride);
     unsigned key = 0xffffffffu;
     bool live = false;
     if (k < sd.np) {
-      const int64_t i = sd.perm ? (int64_t)__ldg(&sd.perm[k]) : k;   // cell-binned order
-      double f[3];
+      double f[3], xyz[3];
       if (FROM_ARRAY) {
         f[0] = __ldg(&f_in[3 * i]); f[1] = __ldg(&f_in[3 * i + 1]); f[2] = __ldg(&f_in[3 * i + 2]);
+        xyz[0] = __ldg(&sd.X[3 * i + 0]); xyz[1] = __ldg(&sd.X[3 * i + 1]); xyz[2] = __ldg(&sd.X[3 * i + 2]);
       } else {
-        point_force(sd, pt, i, f);
+        point_force(sd, pt, i, f, xyz);
       }
       live = (f[0] != 0.0) || (f[1] != 0.0) || (f[2] != 0.0);
-      const int jx = axis_weights(__ldg(&sd.X[3 * i + 0]), g.invh, r + 0) & (N1 - 1);
-      const int jy = axis_weights(__ldg(&sd.X[3 * i + 1]), g.invh, r + 4) & (N2 - 1);
-      const int jz = axis_weights(__ldg(&sd.X[3 * i + 2]), g.invh, r + 8) & (N3 - 1);
-      r[12] = f[0] * ih3; r[13] = f[1] * ih3; r[14] = f[2] * ih3;
+      double wx[4], wy[4], wz[4];
+      const int jx = axis_weights(xyz[0], g.invh, wx) & (N1 - 1);
+      const int jy = axis_weights(xyz[1], g.invh, wy) & (N2 - 1);
+      const int jz = axis_weights(xyz[2], g.invh, wz) & (N3 - 1);
+      double2 *rw = reinterpret_cast<double2 *>(r);
+#pragma unroll
+      for (int bb = 0; bb < 4; ++bb) {
+        rw[2 * bb] = make_double2(wx[0] * wy[bb], wx[1] * wy[bb]);
+        rw[2 * bb + 1] = make_double2(wx[2] * wy[bb], wx[3] * wy[bb]);
+      }
+      const double f0 = f[0] * ih3, f1 = f[1] * ih3, f2 = f[2] * ih3;
+      double2 *rg = reinterpret_cast<double2 *>(r + 16);
+      rg[0] = make_double2(f0 * wz[0], f1 * wz[0]); rg[1] = make_double2(f2 * wz[0], f0 * wz[2]);
+      rg[2] = make_double2(f1 * wz[2], f2 * wz[2]); rg[3] = make_double2(f0 * wz[1], f1 * wz[1]);
+      rg[4] = make_double2(f2 * wz[1], f0 * wz[3]); rg[5] = make_double2(f1 * wz[3], f2 * wz[3]);
       key = ((unsigned)jz * N2 + (unsigned)jy) * N1 + (unsigned)jx;
     }
     __syncwarp();
@@ -271,12 +297,13 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
         const int p2 = m ? __ffs(m) - 1 : 32;
         m &= m - 1;
         const double *q = rec[warp][p], *q2 = rec[warp][p2];
-        const double wab = q[a] * q[4 + b], wab2 = q2[a] * q2[4 + b];
-        const double w0 = wab * q[8 + c0], w1 = wab * q[10 + c0];
-        const double v0 = wab2 * q2[8 + c0], v1 = wab2 * q2[10 + c0];
-        acc[0] += q[12] * w0 + q2[12] * v0; acc[1] += q[12] * w1 + q2[12] * v1;
-        acc[2] += q[13] * w0 + q2[13] * v0; acc[3] += q[13] * w1 + q2[13] * v1;
-        acc[4] += q[14] * w0 + q2[14] * v0; acc[5] += q[14] * w1 + q2[14] * v1;
+        const double w = q[ab], w2 = q2[ab];
+        const double2 *g = reinterpret_cast<const double2 *>(q + 16 + 6 * c0);
+        const double2 *g2 = reinterpret_cast<const double2 *>(q2 + 16 + 6 * c0);
+        const double2 u0 = g[0], u1 = g[1], u2 = g[2], v0 = g2[0], v1 = g2[1], v2 = g2[2];
+        acc[0] += w * u0.x + w2 * v0.x; acc[2] += w * u0.y + w2 * v0.y;
+        acc[4] += w * u1.x + w2 * v1.x; acc[1] += w * u1.y + w2 * v1.y;
+        acc[3] += w * u2.x + w2 * v2.x; acc[5] += w * u2.y + w2 * v2.y;
       }
       const unsigned jx = kl & (N1 - 1), jy = (kl >> lg1) & (N2 - 1), jz = kl >> (lg1 + lg2);
       const size_t x = (jx + a) & (N1 - 1), y = (jy + b) & (N2 - 1);
