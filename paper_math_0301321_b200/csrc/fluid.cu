@@ -194,7 +194,9 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   }
   auto ld = [&](int e, int slot) { return rr[slot]; };
   double2 *sp = sm + pencil * LD;
-  auto sst = [sp](int e, double2 v) { sp[PAD(e)] = v; };
+  // the last pass stores unswizzled (consecutive e per quarter-warp): the split below then
+  // reads both k and M - k runs without bank conflicts
+  auto sst = [sp](int e, double2 v) { sp[e] = v; };
   auto bar = []() { __syncthreads(); };             // u tile dead before pencils alias it
   fft_io<M, -1, false, true>(sp, t, twM, ld, sst, bar);
   __syncthreads();
@@ -206,8 +208,8 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   for (int idx = threadIdx.x; idx < NC * RB * H; idx += blockDim.x) {
     const int pc = idx / H, k = idx % H;
     const int cp = pc / RB, rw = pc % RB;
-    const double2 Zk = sm[pc * LD + PAD(k)];
-    const double2 Zm = sm[pc * LD + PAD((M - k) & (M - 1))];
+    const double2 Zk = sm[pc * LD + k];
+    const double2 Zm = sm[pc * LD + ((M - k) & (M - 1))];
     const double2 E = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y - Zm.y));
     const double2 O = make_double2(0.5 * (Zk.y + Zm.y), -0.5 * (Zk.x - Zm.x));
     const double2 wO = cmul(__ldg(&twN[k]), O);

@@ -162,6 +162,11 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   // keeps every tile access an LDS/STS (a uintptr_t round trip would make them generic)
   double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
   const int ntiles = NB * W * (NC == 1 ? 3 : 1);      // NC = 1: (kx block, w, comp) tiles
+  // z symbols (sin and sin^2 terms along the pencil) staged once: the solve reads them per
+  // element, an L1/L2 latency the loop would otherwise expose on every iteration
+  __shared__ double symz[MODE == MODE_Z ? 2 * N : 1];
+  if constexpr (MODE == MODE_Z)
+    for (int k = threadIdx.x; k < N; k += blockDim.x) { symz[k] = sym.sz[k]; symz[N + k] = sym.lz[k]; }
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
     fence_mbar_init();
@@ -244,12 +249,11 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
       const bool live = kx <= M;
       const double sx = live ? sym.sx[kx] : 0.0, lxy = (live ? sym.lx[kx] : 0.0) + ly;
       const bool nxy = ny && (kx == 0 || kx == M);
-      for (int kz = gtid / C; live && kz < N; kz += NTG / C) {
-        double2 *q0 = buf + swz<C>(kz, c);
+      // û = (r̂ - s (s.r̂)/|s|^2)/d, p̂ = -i (s.r̂)/|s|^2; null modes (Z6): û = r̂/d
+      auto solve = [&](int kz, double2 *q0, double2 r0, double2 r1, double2 r2) {
         double2 *q1 = q0 + K::TILE, *q2 = q1 + K::TILE;
-        const double2 r0 = *q0, r1 = *q1, r2 = *q2;
-        const double sz = sym.sz[kz];
-        const double d = cdt + g.mu * (lxy + sym.lz[kz]);
+        const double sz = symz[kz];
+        const double d = cdt + g.mu * (lxy + symz[N + kz]);
         const bool nul = nxy && (kz == 0 || 2 * kz == N);
         if (nul) {                                       // reading Z6
           const double inv = invV / d;
@@ -267,6 +271,10 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
           *q2 = make_double2((r2.x - sz * q.x) * inv, (r2.y - sz * q.y) * inv);
           if (pspec) pspec[((size_t)ky * N + kz) * g.P + kx] = make_double2(q.y * invV, -q.x * invV);
         }
+      };
+      for (int kz = gtid / C; live && kz < N; kz += NTG / C) {
+        double2 *q0 = buf + swz<C>(kz, c);
+        solve(kz, q0, q0[0], q0[K::TILE], q0[2 * K::TILE]);
       }
       named_bar(bar, NTG);
       fft_inplace<N, +1, C>(A, t, twN, bar, NTG);
