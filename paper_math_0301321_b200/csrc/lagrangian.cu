@@ -357,7 +357,7 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
 // ------------------------------------------------------------------ interp + update
 // U = sum_c wz_c sum_b wy_b (sum_a wx_a u(jx+a, jy+b, jz+c)) straight from global memory
 // (row sums first, 32-bit cell offsets; a row with no periodic wrap in x is 4 consecutive
-// doubles off one base pointer).  Used by warps whose points span more than BOXES boxes.
+// doubles off one base pointer).  Used by warps whose points span more than IMMA_MAXG boxes.
 __device__ __forceinline__ void interp_direct(const double *__restrict__ u, int N1, int N2,
                                               int N3, int Vi,
                                               int jx, int jy, int jz, const double wx[4],
@@ -404,19 +404,36 @@ __device__ __forceinline__ void interp_direct(const double *__restrict__ u, int 
   }
 }
 
-// One thread per point in cell-binned order.  A warp whose 32 points use at most BOXES
-// distinct 4x4x4 support boxes (the common case after binning) loads each box once,
-// cooperatively (lane = (a, b, c0): nodes (a, b, c0) and (a, b, c0 + 2), 3 components),
-// into shared memory; each lane then sums its point from its box with broadcast reads.
-// Other warps gather straight from global memory.  Update X^{n+1} = X^n + dt U fused;
-// non-finite flag.
-constexpr int INTERP_THREADS = 128, BOXES = 4, BOXLD = 3 * 64 + 2;   // +2: bank shift per box
+constexpr int INTERP_THREADS = 128;
 
-__global__ void __launch_bounds__(INTERP_THREADS)
-k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
-         long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm,
-         const uint8_t *__restrict__ fixed) {
-  __shared__ double box[INTERP_THREADS / 32][BOXES][BOXLD];
+// One thread per point in cell-binned order; X^{n+1} = X^n + dt U fused; non-finite flag.
+// Per group of lanes whose points share a support box (same base cell), the x contraction of all members is one fp64 MMA per 8 output columns:
+//   S[p][(comp, c, b)] = sum_a wx_p[a] u(jx + a, jy + b, jz + c)[comp]
+// (M = 8 members, K = 4 nodes along x, N = 48 columns = 6 m8n8k4 tiles).  The B fragments
+// (lane = (a, b, c1): u at c1 and c1 + 2, 3 components) are gathered once per group
+// straight into registers — no shared-memory box; the A fragments are the members' x
+// weights.  Each lane of a D row then weighs its 12 values by wy[b] wz[c] and the 4 lanes
+// of the row reduce with two xor shuffles.  Warps spanning more than IMMA_MAXG boxes gather
+// per point (interp_direct).
+constexpr int IMMA_MAXG = 8;
+
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
+               : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(0.0), "d"(0.0));
+}
+
+// 8 blocks (32 warps) per SM, <= 64 registers: the gathers want the occupancy (117 us at
+// cfg4; 6 blocks 126 us, uncapped 250 us)
+#ifndef IBK_IMINB
+#define IBK_IMINB 8
+#endif
+__global__ void __launch_bounds__(INTERP_THREADS, IBK_IMINB)
+k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
+             long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm,
+             const uint8_t *__restrict__ fixed) {
+  // per lane-point: wx[0..3] | wy[0..3] | wz[0], wz[2], wz[1], wz[3]  (+2 pad: odd 16-B stride)
+  __shared__ __align__(16) double rec[INTERP_THREADS / 32][32][14];
+  __shared__ double uo[INTERP_THREADS / 32][32][3];
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
@@ -434,42 +451,59 @@ k_interp(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, doubl
   const unsigned active = __ballot_sync(0xffffffffu, live);
   const unsigned peers = __match_any_sync(0xffffffffu, live ? key : 0xffffffffu) & active;
   const unsigned leaders = __ballot_sync(0xffffffffu, live && lane == __ffs(peers) - 1);
-  double U0, U1, U2;
-  if (__popc(leaders) <= BOXES) {
-    const int a = lane & 3, b = (lane >> 2) & 3, c0 = lane >> 4;
+  double U0 = 0.0, U1 = 0.0, U2 = 0.0;
+  if (__popc(leaders) <= IMMA_MAXG) {
+    double2 *rw = reinterpret_cast<double2 *>(rec[warp][lane]);
+    rw[0] = make_double2(wx[0], wx[1]); rw[1] = make_double2(wx[2], wx[3]);
+    rw[2] = make_double2(wy[0], wy[1]); rw[3] = make_double2(wy[2], wy[3]);
+    rw[4] = make_double2(wz[0], wz[2]); rw[5] = make_double2(wz[1], wz[3]);
+    __syncwarp();
+    const int a = lane & 3, b = (lane >> 2) & 3, c1 = lane >> 4;     // B fragment node
+    const int p = lane >> 2, q = lane & 3;                            // D row, column pair
+    const int yb = 2 * (q & 1), zc = q >> 1;                          // epilogue wy / wz pair
     unsigned lm = leaders;
-    for (int gi = 0; lm; ++gi) {
+    while (lm) {
       const int ld = __ffs(lm) - 1;
       lm &= lm - 1;
+      const unsigned kl = __shfl_sync(0xffffffffu, key, ld);   // every lane shuffles
+      const unsigned gm = __ballot_sync(0xffffffffu, live && key == kl);
       const int gx = __shfl_sync(0xffffffffu, jx, ld), gy = __shfl_sync(0xffffffffu, jy, ld),
                 gz = __shfl_sync(0xffffffffu, jz, ld);
       const int xo = (gx + a) & (N1 - 1), yo = (gy + b) & (N2 - 1);
-      double *bx = box[warp][gi];
+      const int e0 = (((gz + c1) & (N3 - 1)) * N2 + yo) * N1 + xo;
+      const int e1 = (((gz + c1 + 2) & (N3 - 1)) * N2 + yo) * N1 + xo;
+      // tile t: component t / 2, c = c1 (t even) or c1 + 2 (t odd)
+      double bf[6];
+      bf[0] = __ldg(u + e0);          bf[1] = __ldg(u + e1);
+      bf[2] = __ldg(u + Vi + e0);     bf[3] = __ldg(u + Vi + e1);
+      bf[4] = __ldg(u + 2 * Vi + e0); bf[5] = __ldg(u + 2 * Vi + e1);
+      const int nm = __popc(gm);
+      for (int m0 = 0; m0 < nm; m0 += 8) {
+        const int src = m0 + p < nm ? (int)__fns(gm, 0, m0 + p + 1) : -1;
+        const double af = src >= 0 ? rec[warp][src][a] : 0.0;
+        double d[6][2];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = c0 + 2 * h;
-        const int cell = (((gz + c) & (N3 - 1)) * N2 + yo) * N1 + xo;
-        const int node = (c * 4 + b) * 4 + a;
-        bx[node] = __ldg(u + cell);
-        bx[64 + node] = __ldg(u + Vi + cell);
-        bx[128 + node] = __ldg(u + 2 * Vi + cell);
+        for (int t = 0; t < 6; ++t) dmma_8x8x4(d[t][0], d[t][1], af, bf[t]);
+        // D[p][n], n = 2q + e: b = 2 (q & 1) + e, c = (t & 1) * 2 + (q >> 1); rows past the
+        // group (src < 0) are zero and read record 0 (all lanes stay in the shuffles)
+        const int sr = src >= 0 ? src : 0;
+        const double2 yy = *reinterpret_cast<const double2 *>(&rec[warp][sr][4 + yb]);
+        const double2 zz = *reinterpret_cast<const double2 *>(&rec[warp][sr][8 + 2 * zc]);
+        double s[3];
+#pragma unroll
+        for (int cp = 0; cp < 3; ++cp)
+          s[cp] = zz.x * (yy.x * d[2 * cp][0] + yy.y * d[2 * cp][1]) +
+                  zz.y * (yy.x * d[2 * cp + 1][0] + yy.y * d[2 * cp + 1][1]);
+#pragma unroll
+        for (int cp = 0; cp < 3; ++cp) {
+          s[cp] += __shfl_xor_sync(0xffffffffu, s[cp], 1, 4);
+          s[cp] += __shfl_xor_sync(0xffffffffu, s[cp], 2, 4);
+        }
+        if (src >= 0 && q == 0) { uo[warp][src][0] = s[0]; uo[warp][src][1] = s[1]; uo[warp][src][2] = s[2]; }
       }
     }
     __syncwarp();
-    const int mine = __popc(leaders & ((1u << (__ffs(peers) - 1)) - 1u));
-    const double *bx = box[warp][live ? mine : 0];
-    U0 = U1 = U2 = 0.0;
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-#pragma unroll
-      for (int bb = 0; bb < 4; ++bb) {
-        const double *r = bx + (c * 4 + bb) * 4;
-        const double s0 = wx[0] * r[0] + wx[1] * r[1] + wx[2] * r[2] + wx[3] * r[3];
-        const double s1 = wx[0] * r[64] + wx[1] * r[65] + wx[2] * r[66] + wx[3] * r[67];
-        const double s2 = wx[0] * r[128] + wx[1] * r[129] + wx[2] * r[130] + wx[3] * r[131];
-        const double wbc = wy[bb] * wz[c];
-        U0 += wbc * s0; U1 += wbc * s1; U2 += wbc * s2;
-      }
+    U0 = uo[warp][lane][0]; U1 = uo[warp][lane][1]; U2 = uo[warp][lane][2];
   } else {
     interp_direct(u, N1, N2, N3, Vi, jx, jy, jz, wx, wy, wz, U0, U1, U2);
   }
@@ -492,7 +526,7 @@ cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_
                           double *U_out, long long *flag, const long long *dev_n, long long n,
                           const int *perm, const uint8_t *fixed, cudaStream_t s) {
   if (np > 0)
-    k_interp<<<(unsigned)((np + INTERP_THREADS - 1) / INTERP_THREADS), INTERP_THREADS, 0, s>>>(
+    k_interp_mma<<<(unsigned)((np + INTERP_THREADS - 1) / INTERP_THREADS), INTERP_THREADS, 0, s>>>(
         g, u, X, np, U_out, flag, dev_n, n, perm, fixed);
   return cudaGetLastError();
 }
