@@ -210,6 +210,14 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
   }
 }
 
+// ------------------------------------------------------------------ fp64 tensor-core MMA
+// D (8x8) = A (8x4) B (4x8), fp64 (DMMA).  Fragments (PTX m8n8k4 .f64): lane l holds
+// A[l >> 2][l & 3], B[l & 3][l >> 2] and D[l >> 2][2 (l & 3) + {0, 1}].
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
+               : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(0.0), "d"(0.0));
+}
+
 // ------------------------------------------------------------------ force + spread
 #ifndef IBK_SPT
 #define IBK_SPT 128
@@ -416,11 +424,6 @@ constexpr int INTERP_THREADS = 128;
 // of the row reduce with two xor shuffles.  Warps spanning more than IMMA_MAXG boxes gather
 // per point (interp_direct).
 constexpr int IMMA_MAXG = 8;
-
-__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%4, %5};\n"
-               : "=d"(d0), "=d"(d1) : "d"(a), "d"(b), "d"(0.0), "d"(0.0));
-}
 
 // 8 blocks (32 warps) per SM, <= 64 registers: the gathers want the occupancy (117 us at
 // cfg4; 6 blocks 126 us, uncapped 250 us)
