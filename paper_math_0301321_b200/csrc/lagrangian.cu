@@ -519,7 +519,8 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
       bad = !(isfinite(y0) && isfinite(y1) && isfinite(y2));
     }
   }
-  if (flag && __syncthreads_or(bad) && threadIdx.x == 0) {
+  // warp-level vote: a block-wide barrier here made every warp wait for the block's slowest
+  if (flag && __any_sync(0xffffffffu, bad) && lane == 0) {
     const long long st = dev_n ? *dev_n : n;
     atomicMin(flag, st);
   }

@@ -23,11 +23,15 @@ template <int N>
 struct XT {
   static constexpr int M = N / 2;
   static constexpr int T = Plan<M>::T;                  // threads per pencil
-  // 3 groups of 3 warps + the producer = 10 warps: <= 204 registers per thread, so the
-  // FFT state never spills (spills would miss the small L1 left beside ~200 KB of smem)
+  // 2 groups of 3 warps + the producer = 7 warps: the FFT state never spills (spills would
+  // miss the small L1 left beside the smem ring).  Measured at 256^3: 2 groups 138 us,
+  // 3 groups 142 us, 4 groups 156 us (register-capped), 1 group 160 us.
   static constexpr int RB = 32 / T < N ? 32 / T : N;    // rows per tile
   static constexpr int NTG = 3 * RB * T;                // consumer threads per group
-  static constexpr int G = 3;
+#ifndef IBK_XIG
+#define IBK_XIG 2
+#endif
+  static constexpr int G = IBK_XIG;
   static constexpr int NT = G * NTG;
   static constexpr int NTHR = NT + 32;
   static constexpr int LD = Plan<M>::LD;
@@ -35,7 +39,10 @@ struct XT {
   static constexpr int NQ = RB > 8 ? RB : 8;         // Nyquist slot stride (128-B aligned)
   static constexpr size_t XI = (size_t)3 * RB * N * 8 + 3 * NQ * 16; // xinv S1 rows + Nyquist
   static constexpr size_t SI = ((XI > PENC ? XI : PENC) + 1023) & ~(size_t)1023;
-  static constexpr int SI_STAGES = 6;
+#ifndef IBK_XIS
+#define IBK_XIS 6
+#endif
+  static constexpr int SI_STAGES = IBK_XIS;
   // a TMA box is at most 256 doubles wide: rows of N = 512 doubles arrive as HALVES boxes of
   // HC complex each, stored [comp][half][row][HC]
   static constexpr int BOXC = N < 256 ? N : 256;        // doubles per box row
@@ -69,6 +76,10 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
     fence_mbar_init();
   }
   if (threadIdx.x < G) bad_any[threadIdx.x] = 0;
+  // C2R pre-twiddles staged once per CTA (persistent): shared loads in the pass-0 gather
+  // instead of L1 hits on the table
+  __shared__ double2 twx[M];
+  for (int e = threadIdx.x; e < M; e += blockDim.x) twx[e] = twN[e];
   __syncthreads();
 
   if (threadIdx.x >= K::NT) {                             // -------------- producer warp
@@ -116,7 +127,7 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
       if (e == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real
       const double2 A = make_double2(Xk.x + Xm.x, Xk.y - Xm.y);
       const double2 B = make_double2(Xk.x - Xm.x, Xk.y + Xm.y);
-      const double2 cB = cmul(cconj(__ldg(&twN[e])), B);
+      const double2 cB = cmul(cconj(twx[e]), B);
       return make_double2(A.x - cB.y, A.y + cB.x);
     };
     auto st = [&](int k, double2 v) {
