@@ -104,7 +104,15 @@ __device__ __forceinline__ void dft_reg(double2 *v) {
 
 template <int SIGN>
 __device__ __forceinline__ double2 twiddle(const double2 *__restrict__ tw, int t) {
-  double2 w = __ldg(&tw[t]);
+  double2 w = __ldg(&tw[t]);         // device table (read-only path)
+  if (SIGN > 0) w.y = -w.y;
+  return w;
+}
+// A twiddle table staged in shared memory (persistent kernels that keep it per CTA).
+struct SmemTw { const double2 *p; };
+template <int SIGN>
+__device__ __forceinline__ double2 twiddle(SmemTw tw, int t) {
+  double2 w = tw.p[t];
   if (SIGN > 0) w.y = -w.y;
   return w;
 }
@@ -166,8 +174,8 @@ struct PassI {
   static constexpr int R = P::radix(PASS), NS = P::ns(PASS), NR = L / R, J = NR / P::T;
 };
 
-template <int L, int SIGN, int PASS, class LDF>
-__device__ __forceinline__ void pass_lc(double2 *v, int t, const double2 *__restrict__ tw, LDF ld) {
+template <int L, int SIGN, int PASS, class TW, class LDF>
+__device__ __forceinline__ void pass_lc(double2 *v, int t, TW tw, LDF ld) {
   using I = PassI<L, PASS>;
 #pragma unroll
   for (int q = 0; q < I::J; ++q) {

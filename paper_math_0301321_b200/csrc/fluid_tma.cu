@@ -119,8 +119,8 @@ __device__ __forceinline__ void pass_st_flip(const double2 *v, int t, STF st) {
 
 // In-place length-L Stockham transform of the pencil accessed by A(e) (a double2&), by its
 // T threads; every thread of the consumer group must call it (named barrier BAR, NTG).
-template <int L, int SIGN, int C, class ACC>
-__device__ __forceinline__ void fft_inplace(ACC A, int t, const double2 *__restrict__ tw,
+template <int L, int SIGN, int C, class ACC, class TW>
+__device__ __forceinline__ void fft_inplace(ACC A, int t, TW tw,
                                             int bar, int ntg) {
   double2 v[Plan<L>::RMAX];
   auto ld = [&](int e) { return A(e); };
@@ -167,6 +167,17 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   __shared__ double symz[MODE == MODE_Z ? 2 * N : 1];
   if constexpr (MODE == MODE_Z)
     for (int k = threadIdx.x; k < N; k += blockDim.x) { symz[k] = sym.sz[k]; symz[N + k] = sym.lz[k]; }
+  // z modes: twiddles staged likewise (one copy per persistent CTA; 2511 -> 2316 us at
+  // 512^3, neutral at 256^3).  The y modes keep the read-only global path: their shared
+  // memory is busier and staged twiddles slowed them (139 -> 174 us at 256^3).
+  constexpr bool ZM = ColCfg<N, MODE>::ZM;
+  __shared__ double2 tws[ZM ? N : 1];
+  if constexpr (ZM)
+    for (int k = threadIdx.x; k < N; k += blockDim.x) tws[k] = twN[k];
+  const auto tw = [&]() {
+    if constexpr (ZM) return SmemTw{tws};
+    else return twN;
+  }();
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
     fence_mbar_init();
@@ -239,7 +250,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
     double2 *pc = buf + comp * K::TILE;
     auto A = [pc, col](int e) -> double2 & { return pc[swz<C>(e, col)]; };
     if (MODE == MODE_Z) {
-      fft_inplace<N, -1, C>(A, t, twN, bar, NTG);
+      fft_inplace<N, -1, C>(A, t, tw, bar, NTG);
       const int kx0 = C * cw.x, ky = cw.w;               // NC = 3 here
       const double sy = sym.sy[ky], ly = sym.ly[ky];
       const bool ny = (ky == 0) || (2 * ky == g.N2);
@@ -277,9 +288,9 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
         solve(kz, q0, q0[0], q0[K::TILE], q0[2 * K::TILE]);
       }
       named_bar(bar, NTG);
-      fft_inplace<N, +1, C>(A, t, twN, bar, NTG);
+      fft_inplace<N, +1, C>(A, t, tw, bar, NTG);
     } else {
-      fft_inplace<N, (MODE == MODE_YINV || MODE == MODE_ZINV) ? +1 : -1, C>(A, t, twN, bar, NTG);
+      fft_inplace<N, (MODE == MODE_YINV || MODE == MODE_ZINV) ? +1 : -1, C>(A, t, tw, bar, NTG);
     }
     fence_proxy_async();                                 // generic writes -> TMA store
     named_bar(bar, NTG);
