@@ -93,10 +93,11 @@ cudaError_t init_tables(ib_ctx *c) {
 // shared memory with cp.async; each thread then computes r at the 2*RMAX cells of its
 // first-pass elements (z_e = r_2e + i r_2e+1) from that tile plus the z +- 1 rows (L2),
 // straight into registers.  The tile is then reused as the FFT exchange buffer.
-// 5 CTAs (15 warps) per SM: <= 128 registers, 4 resident warps per scheduler (266 vs 287 us
-// at 256^3 with 4 CTAs; 6 CTAs spill)
+// CTAs per SM the registers must allow: 5 (15 warps, <= 128 registers) at N1 <= 256 (266
+// vs 287 us at 256^3 with 4; 6 spill); 4 at N1 = 512, whose 48 KB tiles fit only 4 per SM
+// anyway (2407 vs 2620 us at 512^3 with the 128-register cap)
 #ifndef IBK_XMINB
-#define IBK_XMINB 5
+#define IBK_XMINB (N >= 512 ? 4 : 5)
 #endif
 template <int N, int MODE>
 __global__ void __launch_bounds__(3 * XCfg<N>::RB * XCfg<N>::T, IBK_XMINB)
