@@ -120,6 +120,45 @@ def test_interp_matches_oracle_and_adjoint(ibm, olib, N, npts):
     assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
 
 
+def _clustered_points(N, rng):
+    """Points laid out warp by warp (index order) so that the tensor-core interp sees every
+    grouping case: one 32-member group (4 MMA row blocks), uneven groups (9, 8, 7, 5, 3),
+    exactly 8 groups (the MMA limit), 9 groups (per-point fallback), cells on the periodic
+    edge (wrapped support), and a partial last warp (non-live lanes)."""
+    h = 1.0 / N
+    warps = [[32], [9, 8, 7, 5, 3], [4] * 8, [3, 3, 3, 3, 4, 4, 4, 4, 4], [13, 7]]
+    pts = []
+    cell = 0
+    for sizes in warps:
+        for m in sizes:
+            c = np.array([(7 * cell) % N, (3 * cell + 1) % N, (5 * cell + 2) % N])
+            if cell % 3 == 0:
+                c[cell % 3] = N - 1                 # support wraps around the box
+            cell += 1
+            pts.append((c + rng.uniform(0.0, 1.0, size=(m, 3))) * h)
+    return np.ascontiguousarray(np.concatenate(pts))
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_interp_grouping_cases_match_oracle(ibm, olib, shuffle):
+    N = 32
+    rng = np.random.default_rng(11)
+    X = _clustered_points(N, rng)
+    if shuffle:
+        X = X[rng.permutation(X.shape[0])]
+    u = rng.standard_normal((3, N, N, N))
+    patches, st = _points_only(X)
+    with _ctx(ibm, N, X=X, patches=patches, stiff=st) as c:
+        U = c.debug_interp(u)
+        f = rng.standard_normal((X.shape[0], 3))
+        F = c.debug_spread(f)
+    ref = olib.interp(N, 1.0 / N, u, X)
+    assert rel_l2(U, ref) < 1e-14
+    assert np.max(np.abs(U - ref)) <= 1e-13 * np.max(np.abs(ref))
+    Fo = olib.spread(N, 1.0 / N, X, f)
+    assert rel_l2(F, Fo) < 1e-13
+
+
 @pytest.mark.parametrize("step", [0, 3, 5])
 def test_force_matches_oracle(ibm, olib, step):
     cfg = small_sheet_config(N=16, n1=12, n2=10, seed=5)
