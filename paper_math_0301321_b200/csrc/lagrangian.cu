@@ -425,8 +425,8 @@ constexpr int INTERP_THREADS = 128;
 // per point (interp_direct).
 constexpr int IMMA_MAXG = 8;
 
-// 8 blocks (32 warps) per SM, <= 64 registers: the gathers want the occupancy (117 us at
-// cfg4; 6 blocks 126 us, uncapped 250 us)
+// 8 blocks (32 warps) per SM, <= 64 registers: the gathers want the occupancy (109 us at
+// cfg4; 7 blocks 111 us, 6 blocks 113 us, uncapped 250 us)
 #ifndef IBK_IMINB
 #define IBK_IMINB 8
 #endif
@@ -437,6 +437,7 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
   // per lane-point: wx[0..3] | wy[0..3] | wz[0], wz[2], wz[1], wz[3]  (+2 pad: odd 16-B stride)
   __shared__ __align__(16) double rec[INTERP_THREADS / 32][32][14];
   __shared__ double uo[INTERP_THREADS / 32][32][3];
+  __shared__ unsigned char mlist[INTERP_THREADS / 32][32];   // lanes of the current group
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
@@ -481,8 +482,11 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
       bf[2] = __ldg(u + Vi + e0);     bf[3] = __ldg(u + Vi + e1);
       bf[4] = __ldg(u + 2 * Vi + e0); bf[5] = __ldg(u + 2 * Vi + e1);
       const int nm = __popc(gm);
+      __syncwarp();                                     // previous group's list consumed
+      if ((gm >> lane) & 1u) mlist[warp][__popc(gm & ((1u << lane) - 1u))] = (unsigned char)lane;
+      __syncwarp();
       for (int m0 = 0; m0 < nm; m0 += 8) {
-        const int src = m0 + p < nm ? (int)__fns(gm, 0, m0 + p + 1) : -1;
+        const int src = m0 + p < nm ? (int)mlist[warp][m0 + p] : -1;
         const double af = src >= 0 ? rec[warp][src][a] : 0.0;
         double d[6][2];
 #pragma unroll
@@ -497,12 +501,15 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
         for (int cp = 0; cp < 3; ++cp)
           s[cp] = zz.x * (yy.x * d[2 * cp][0] + yy.y * d[2 * cp][1]) +
                   zz.y * (yy.x * d[2 * cp + 1][0] + yy.y * d[2 * cp + 1][1]);
-#pragma unroll
-        for (int cp = 0; cp < 3; ++cp) {
-          s[cp] += __shfl_xor_sync(0xffffffffu, s[cp], 1, 4);
-          s[cp] += __shfl_xor_sync(0xffffffffu, s[cp], 2, 4);
-        }
-        if (src >= 0 && q == 0) { uo[warp][src][0] = s[0]; uo[warp][src][1] = s[1]; uo[warp][src][2] = s[2]; }
+        // transpose-reduce over the row's 4 lanes (3 shuffles): lane q ends with component
+        // 2 (q & 1) + (q >> 1) summed over the row (q = 3: the zero pad)
+        const bool o1 = q & 1, o2 = q & 2;
+        const double ra = __shfl_xor_sync(0xffffffffu, o1 ? s[0] : s[2], 1, 4);
+        const double rb = __shfl_xor_sync(0xffffffffu, o1 ? s[1] : 0.0, 1, 4);
+        const double ka = (o1 ? s[2] : s[0]) + ra, kb = (o1 ? 0.0 : s[1]) + rb;
+        const double sum = (o2 ? kb : ka) + __shfl_xor_sync(0xffffffffu, o2 ? ka : kb, 2, 4);
+        const int cq = 2 * (q & 1) + (q >> 1);
+        if (src >= 0 && cq < 3) uo[warp][src][cq] = sum;
       }
     }
     __syncwarp();
