@@ -309,9 +309,10 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
         const double2 *g = reinterpret_cast<const double2 *>(q + 16 + 6 * c0);
         const double2 *g2 = reinterpret_cast<const double2 *>(q2 + 16 + 6 * c0);
         const double2 u0 = g[0], u1 = g[1], u2 = g[2], v0 = g2[0], v1 = g2[1], v2 = g2[2];
-        acc[0] += w * u0.x + w2 * v0.x; acc[2] += w * u0.y + w2 * v0.y;
-        acc[4] += w * u1.x + w2 * v1.x; acc[1] += w * u1.y + w2 * v1.y;
-        acc[3] += w * u2.x + w2 * v2.x; acc[5] += w * u2.y + w2 * v2.y;
+        // two fused multiply-adds per accumulator (acc += w u + w2 v contracts to 3 ops)
+        acc[0] = fma(w2, v0.x, fma(w, u0.x, acc[0])); acc[2] = fma(w2, v0.y, fma(w, u0.y, acc[2]));
+        acc[4] = fma(w2, v1.x, fma(w, u1.x, acc[4])); acc[1] = fma(w2, v1.y, fma(w, u1.y, acc[1]));
+        acc[3] = fma(w2, v2.x, fma(w, u2.x, acc[3])); acc[5] = fma(w2, v2.y, fma(w, u2.y, acc[5]));
       }
       const unsigned jx = kl & (N1 - 1), jy = (kl >> lg1) & (N2 - 1), jz = kl >> (lg1 + lg2);
       const size_t x = (jx + a) & (N1 - 1), y = (jy + b) & (N2 - 1);
