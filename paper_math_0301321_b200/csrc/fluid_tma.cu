@@ -63,7 +63,12 @@ template <int N, int MODE> struct ColCfg {
   static constexpr int G = ZM ? (N == 128 || N == 256 ? 2 : 1) : (N >= 512 ? 1 : (N == 256 ? 1 : 4));
 #else
   static constexpr int NC = ZM ? 3 : 1;
-  static constexpr int G = ZM ? (N == 256 ? 2 : (N <= 128 ? IBK_ZG128 : 1)) : (N >= 512 ? 1 : (N == 256 ? IBK_YG256 : 4));
+// z pass at N3 = 256: 3 consumer groups (19 warps, <= 96 registers with a small spill) hide
+// the shared-memory latency best: 201 us vs 218 (2 groups), 316 (1), 290 (4, heavy spills)
+#ifndef IBK_ZG256
+#define IBK_ZG256 3
+#endif
+  static constexpr int G = ZM ? (N == 256 ? IBK_ZG256 : (N <= 128 ? IBK_ZG128 : 1)) : (N >= 512 ? 1 : (N == 256 ? IBK_YG256 : 4));
 #endif
   static constexpr size_t SB = (size_t)NC * N * C * 16;
   static constexpr int S0 = (int)((200 * 1024) / SB);
