@@ -81,6 +81,14 @@ def main():
         lines = [f"# ncu --metrics gpu__time_duration.sum --clock-control none ({tag})",
                  "# cold-cache, serialised launches: compare SHARES, not absolute times",
                  f"{'us':>9} {'share':>6}  stage / kernel"]
+        if len(L) > 20:           # a whole bench run: per-stage shares first
+            agg, cnt = {}, {}
+            for k, t in L:
+                agg[stage(k)] = agg.get(stage(k), 0.0) + t
+                cnt[stage(k)] = cnt.get(stage(k), 0) + 1
+            lines.append("# per stage over all launches (us total, launches, mean us, share)")
+            for st, t in sorted(agg.items(), key=lambda x: -x[1]):
+                lines.append(f"#   {st:16s} {t:10.1f} {cnt[st]:5d} {t / cnt[st]:8.1f} {100 * t / total:5.1f}%")
         for k, t in L:
             lines.append(f"{t:9.1f} {100 * t / total:5.1f}%  {stage(k):14s} {k[:90]}")
         lines.append(f"{total:9.1f}  total over {len(L)} launches")
