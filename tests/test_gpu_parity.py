@@ -325,7 +325,8 @@ def test_config_full_length_stays_finite_and_bounded(ibm, k):
 # N1 x N2 x N3 boxes such as the paper's 256 x 256 x 128 half-cube
 # (PAPER.md 1003-1007).  Shapes mix the TMA column passes (pencil >= 64) with the cp.async
 # pencil kernels (pencil < 64) on each axis.
-ANISO = [(32, 64, 16), (64, 32, 128), (16, 16, 64), (128, 64, 32)]
+ANISO = [(32, 64, 16), (64, 32, 128), (16, 16, 64), (128, 64, 32),
+         (512, 16, 8), (256, 8, 64), (256, 64, 256)]   # 512-wide x rows (two TMA boxes), tuned group counts
 
 
 @pytest.mark.parametrize("shape", ANISO)
