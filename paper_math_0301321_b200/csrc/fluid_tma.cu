@@ -168,6 +168,19 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   // keeps every tile access an LDS/STS (a uintptr_t round trip would make them generic)
   double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
   const int ntiles = NB * W * (NC == 1 ? 3 : 1);      // NC = 1: (kx block, w, comp) tiles
+  // The forward y pass walks each component's planes top-down: the x forward pass wrote
+  // them bottom-up, so the last-written planes are read while still in L2 (-1 us at 256^3;
+  // walking planes outermost with the components inside was +2.4 us per y pass).
+#ifndef IBK_L2ORDER
+#define IBK_L2ORDER 1
+#endif
+  constexpr bool YREV = IBK_L2ORDER && MODE == MODE_YFWD;
+  const int WW = W;
+  auto tile_w = [&](const Walk &t) {
+    if constexpr (YREV) return W - 1 - t.w;
+    else return t.w;
+  };
+  auto tile_c = [&](const Walk &t) { return t.c; };
   // z symbols (sin and sin^2 terms along the pencil) staged once: the solve reads them per
   // element, an L1/L2 latency the loop would otherwise expose on every iteration
   __shared__ double symz[MODE == MODE_Z ? 2 * N : 1];
@@ -198,7 +211,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
       prefetch_tmap(&map_st);
       // tile -> (x offset in doubles, w = ky or z, first component); boxes of BR rows
       auto load = [&](const Walk &t, int s) {
-        const int x = 2 * C * t.x, w = t.w, c0 = NC == 1 ? t.c : 0;
+        const int x = 2 * C * t.x, w = tile_w(t), c0 = NC == 1 ? tile_c(t) : 0;
         double2 *b = stage0 + (size_t)s * NC * K::TILE;
         mbar_expect_tx(&full[s], K::STAGE_BYTES);
         for (int c = 0; c < NC; ++c)
@@ -209,7 +222,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
           }
       };
       auto store = [&](const Walk &t, int s) {
-        const int x = 2 * C * t.x, w = t.w, c0 = NC == 1 ? t.c : 0;
+        const int x = 2 * C * t.x, w = tile_w(t), c0 = NC == 1 ? tile_c(t) : 0;
         const double2 *b = stage0 + (size_t)s * NC * K::TILE;
         for (int c = 0; c < NC; ++c)
           for (int r0 = 0; r0 < N; r0 += BR) {
@@ -219,7 +232,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
           }
         bulk_commit();
       };
-      Walk lw(blockIdx.x, gridDim.x, NB, W), sw(blockIdx.x, gridDim.x, NB, W);
+      Walk lw(blockIdx.x, gridDim.x, NB, WW), sw(blockIdx.x, gridDim.x, NB, WW);
       int i = 0;
       for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++i) {
         const int s = i % S;
@@ -247,7 +260,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   const int grp = threadIdx.x / NTG, gtid = threadIdx.x % NTG, bar = 1 + grp;
   const int col = gtid % C, t = (gtid / C) % T, comp = gtid / (C * T);
   int i = grp;
-  Walk cw(blockIdx.x + grp * gridDim.x, G * gridDim.x, NB, W);
+  Walk cw(blockIdx.x + grp * gridDim.x, G * gridDim.x, NB, WW);
   const double cdt = g.rho / g.dt, invV = 1.0 / (double)g.V;   // solve constants (MODE_Z)
   for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G, cw.next()) {
     const int s = i % S;
