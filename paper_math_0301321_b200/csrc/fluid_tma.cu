@@ -28,8 +28,8 @@ enum { MODE_Z = 0, MODE_YFWD = 1, MODE_YINV = 2, MODE_ZFWD = 3, MODE_ZINV = 4 };
 #ifndef IBK_YG256
 #define IBK_YG256 1
 #endif
-#ifndef IBK_ZG128            // z pass at N3 = 128: 6 groups (95.7 us at 4h vs 100.9 with 4)
-#define IBK_ZG128 6
+#ifndef IBK_ZG128
+#define IBK_ZG128 4
 #endif
 
 // Column tile geometry: C columns (C = 8 -> 128-byte rows, SWIZZLE_128B; C = 4 -> 64-byte
@@ -63,17 +63,23 @@ template <int N, int MODE> struct ColCfg {
   static constexpr int G = ZM ? (N == 128 || N == 256 ? 2 : 1) : (N >= 512 ? 1 : (N == 256 ? 1 : 4));
 #else
   static constexpr int NC = ZM ? 3 : 1;
-// z pass at N3 = 256: 3 consumer groups (19 warps, <= 96 registers with a small spill) hide
-// the shared-memory latency best: 201 us vs 218 (2 groups), 316 (1), 290 (4, heavy spills)
+// z pass at N3 = 256: 2 consumer groups of 6 warps, 4 stages (218 us; 3 groups with the
+// 3 stages the stage/group rule below allows: 226 us; 1 group 316 us)
 #ifndef IBK_ZG256
-#define IBK_ZG256 3
+#define IBK_ZG256 2
 #endif
   static constexpr int G = ZM ? (N == 256 ? IBK_ZG256 : (N == 128 ? IBK_ZG128 : (N < 128 ? 4 : 1)))
                               : (N >= 512 ? 1 : (N == 256 ? IBK_YG256 : 4));
 #endif
   static constexpr size_t SB = (size_t)NC * N * C * 16;
   static constexpr int S0 = (int)((200 * 1024) / SB);
-  static constexpr int S = S0 > 2 * G + 1 ? 2 * G + 1 : S0;
+  // Each stage must always be consumed by the same group (S a multiple of G): a group only
+  // waits for round r + 1 of a stage after it consumed round r itself.  Otherwise a group
+  // could test a stage's mbarrier parity while the round before it (owned by another group)
+  // has not completed yet, and the parity test would pass two phases early.
+  static constexpr int S1 = S0 > 2 * G + 1 ? 2 * G + 1 : S0;
+  static constexpr int S = S1 >= G ? (S1 / G) * G : S1;
+  static_assert(S % G == 0, "stages per consumer group");
   using K = CT<N, C, G, NC, S>;
 };
 
