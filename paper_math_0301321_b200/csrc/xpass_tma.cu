@@ -53,6 +53,8 @@ struct XT {
   static constexpr int BOXC = N < 256 ? N : 256;        // doubles per box row
   static constexpr int HALVES = N / BOXC, HC = BOXC / 2;
   static_assert(NTG % 32 == 0, "whole warps per group");
+  // each ring stage is always consumed by the same group (see fluid_tma.cu ColCfg)
+  static_assert(SI_STAGES % G == 0, "stages per consumer group");
 };
 
 // ------------------------------------------------------------------ x inverse (C2R)
