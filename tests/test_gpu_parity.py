@@ -329,6 +329,20 @@ ANISO = [(32, 64, 16), (64, 32, 128), (16, 16, 64), (128, 64, 32),
          (512, 16, 8), (256, 8, 64), (256, 64, 256)]   # 512-wide x rows (two TMA boxes), tuned group counts
 
 
+@pytest.mark.parametrize("shape", [(256, 64, 256), (128, 128, 128), (64, 64, 64)])
+def test_column_pass_rings_repeatable(ibm, shape):
+    """Regression for the ring-ownership rule of the TMA column passes (fluid_tma.cu ColCfg):
+    with more consumer groups than stages divide, a group could pass a stage's mbarrier
+    parity test one phase early (about 1 run in 60 faulted or went wrong on 256x64x256).
+    Repeat the multi-group FFT passes and require every result to be right."""
+    n1, n2, n3 = shape
+    x = np.random.default_rng(5).standard_normal((n3, n2, n1))
+    ref = np.fft.rfftn(x)
+    with ibm.IBContext(shape, 1.0 / n1, 1.0, 0.01, 1e-3) as c:
+        for _ in range(25):
+            assert rel_l2(c.debug_fft(x), ref) < 1e-13
+
+
 @pytest.mark.parametrize("shape", ANISO)
 def test_fft_anisotropic(ibm, shape):
     n1, n2, n3 = shape
