@@ -8,5 +8,5 @@ recipes in DESIGN.md §3 / SURVEY.md §8(d).
 from .configs import (  # noqa: F401
     WRAP1, WRAP2, STRETCH1, STRETCH2, BEND1, BEND2, TETHER, FAMILIES,
     Patch, Config, make_config, CONFIG_STEPS, random_divfree_velocity,
-    random_points, small_sheet_config, window_config,
+    random_points, small_sheet_config, window_config, decaying_shear_config,
 )

@@ -446,3 +446,19 @@ def window_config(N=32, m: int = 24, seed: int = 0, rho: float = 1.0, mu: float 
     cfg.drive_amp = amp / cfg.drive_idx.size
     cfg.drive_period = period
     return cfg
+
+
+def decaying_shear_config(N=16, m: int = 3, A: float = 1.0, npts: int = 40, seed: int = 0,
+                          rho: float = 1.0, mu: float = 0.1, dt: float = 1e-2) -> Config:
+    """Free points (one patch, no links: F = 0) in the shear mode u = A sin(2 pi m y) e_x
+    sampled on the lattice, y_j = j h (an input only; the closed-form step lives in
+    tests/test_oracle_force_step.py).  Points are seeded uniformly in the box."""
+    rng = np.random.default_rng(seed)
+    n1, n2, n3 = _dims(N)
+    h = 1.0 / n1
+    X = np.ascontiguousarray(rng.uniform(0.0, 1.0, (npts, 3)) * np.array([n1, n2, n3]) * h)
+    u0 = np.zeros((3, n3, n2, n1))
+    u0[0] = A * np.sin(2.0 * np.pi * m * np.arange(n2) / n2)[None, :, None]
+    name = "shear" + ("x".join(str(v) for v in N) if isinstance(N, (tuple, list)) else str(N))
+    return Config(name, N, h, rho, mu, dt, 2, X, [Patch(0, npts, 1, 0, 0)], np.zeros(0), u0=u0,
+                  info={"m": m, "A": A})

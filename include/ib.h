@@ -96,9 +96,11 @@ int ib_set_option(ib_ctx *ctx, int32_t option, int64_t value);
  * (IB_EDEGENERATE) a link whose endpoints coincide at the given positions. */
 int ib_set_structure(ib_ctx *ctx, const double *points, int64_t np, const ib_patch *patches,
                      int32_t npatch, const double *stiffness, int64_t nstiff);
-/* Replace positions only ([np][3], same np as the structure). */
+/* Replace positions only ([np][3], same np as the structure): X^n of PAPER.md 602-605
+ * (the boundary configuration the next step starts from).  Rejects non-finite values. */
 int ib_set_positions(ib_ctx *ctx, const double *points);
-/* Fluid velocity u^n, [3][N3][N2][N1]. */
+/* Fluid velocity u^n on the lattice (PAPER.md 602-605, 632-633), [3][N3][N2][N1], x fastest.
+ * Rejects non-finite values (IB_EINVAL).  Invalidates a pending pressure. */
 int ib_set_velocity(ib_ctx *ctx, const double *u);
 /* External drive (PAPER.md 988-993): F_idx[d] += amp * sin(2 pi n / period) * dir[d] at
  * step n (t^n = n dt).  dir == NULL: surface-normal drive ("orthogonal to the surface of
@@ -113,13 +115,19 @@ int ib_set_drive(ib_ctx *ctx, const int64_t *idx, int64_t n, const double *dir,
  * still exerts its link forces on the fluid.  NULL clears; ib_set_structure clears it. */
 int ib_set_fixed(ib_ctx *ctx, const uint8_t *mask);
 
-/* Advance nsteps time steps; synchronises the stream at the end.  Returns IB_ENONFINITE
- * (ib_last_error names the step) if u or X became non-finite. */
+/* Advance nsteps time steps of PAPER.md 608-628 (force, spread, eq:discreteNS1-2, then
+ * eq:discreteX with u^{n+1} at X^n); n -> n + nsteps.  Synchronises the stream at the end.
+ * Returns IB_ENONFINITE if u or X became non-finite: ib_last_error names the first bad
+ * step; the batch has still run to its end on the device, so u, X and ib_get_step() are
+ * at n + nsteps (the state is garbage from the bad step on; reset it before resuming). */
 int ib_step(ib_ctx *ctx, int32_t nsteps);
 
 /* Copy out u^n ([3][V], V = N1 N2 N3, may be NULL) and p^n ([V], may be NULL; needs
- * IB_OPT_PRESSURE enabled before the last ib_step, else IB_ESTATE). */
+ * IB_OPT_PRESSURE enabled before the last ib_step, else IB_ESTATE): the velocity and
+ * pressure of eq:discreteNS1-2 (PAPER.md 659-675) after the last step; p is the projection's
+ * pressure with its null modes set to 0 (reading Z6). */
 int ib_get_fields(ib_ctx *ctx, double *u, double *p);
+/* Copy out X^n ([np][3], unwrapped) — the boundary positions of eq:discreteX (725-734). */
 int ib_get_positions(ib_ctx *ctx, double *X);
 int64_t ib_get_step(ib_ctx *ctx);
 int ib_set_step(ib_ctx *ctx, int64_t n);

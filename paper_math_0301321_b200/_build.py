@@ -29,19 +29,37 @@ def nvcc() -> str:
 
 
 def build(force: bool = False, verbose: bool = False, extra=None, out: str = None) -> str:
+    """nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo: each .cu compiled to an
+    object in parallel (build/obj*/), then linked into the shared library."""
     target = out or SO
     newest = max(os.path.getmtime(p) for p in _deps())
     if not force and os.path.exists(target) and os.path.getmtime(target) >= newest:
         return target
-    tmp = target + f".tmp{os.getpid()}"
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
-           "-cudart", "shared", "-I", os.path.join(ROOT, "include"), "-o", tmp, *sources()]
+    from concurrent.futures import ThreadPoolExecutor
+    tag = f"{os.getpid()}"
+    odir = os.path.join(HERE, "build", f"obj{tag}")
+    os.makedirs(odir, exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
+             "-I", os.path.join(ROOT, "include")]
     if verbose:
-        cmd.insert(1, "-Xptxas=-v")
+        flags.insert(0, "-Xptxas=-v")
     if extra:
-        cmd[1:1] = list(extra)
-    subprocess.check_call(cmd)
+        flags[0:0] = list(extra)
+    objs = []
+
+    def one(src):
+        o = os.path.join(odir, os.path.basename(src) + ".o")
+        subprocess.check_call([nvcc(), *flags, "-c", "-o", o, src])
+        return o
+
+    with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
+        objs = list(ex.map(one, sources()))
+    tmp = target + f".tmp{tag}"
+    subprocess.check_call([nvcc(), *ARCH, "-shared", "-cudart", "shared", "-o", tmp, *objs])
     os.replace(tmp, target)
+    for o in objs:
+        os.remove(o)
+    os.rmdir(odir)
     return target
 
 

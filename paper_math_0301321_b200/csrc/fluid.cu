@@ -299,12 +299,7 @@ k_ypass(FluidGeom g, const double2 *in, double2 *out, size_t in_zs, size_t in_es
 
 template <class K>
 static int persistent_grid(K kernel, int threads, size_t smem, int ntiles) {
-  static int nsm = 0;
-  if (!nsm) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int nsm = sm_count();
   int per = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
   if (per < 1) per = 1;

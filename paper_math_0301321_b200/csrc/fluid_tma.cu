@@ -270,6 +270,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   const double cdt = g.rho / g.dt, invV = 1.0 / (double)g.V;   // solve constants (MODE_Z)
   for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G, cw.next()) {
     const int s = i % S;
+    if (s % G != grp) __trap();                          // ring-ownership rule (ColCfg)
     mbar_wait(&full[s], (i / S) & 1);
     double2 *buf = stage0 + (size_t)s * NC * K::TILE;
     double2 *pc = buf + comp * K::TILE;
@@ -396,9 +397,8 @@ cudaError_t colfft_make_maps(const FluidGeom &g, double2 *spec, double2 *spec2, 
 
 template <class Kern>
 static int one_per_sm_grid(Kern k, int threads, size_t smem, int ntiles) {
-  int dev = 0, nsm = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int per = 0;
+  const int nsm = sm_count();
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, threads, smem);
   if (per < 1) per = 1;
   return ntiles < per * nsm ? ntiles : per * nsm;
@@ -409,12 +409,13 @@ static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
                                    const CUtensorMap &st, double2 *pspec, const double2 *twN,
                                    const Sym &sym, cudaStream_t s) {
   using K = typename ColCfg<N, MODE>::K;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  const int dev = current_device();
+  if (!attr.done(dev)) {
     cudaError_t e = cudaFuncSetAttribute(k_colfft<N, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)K::SMEM);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.mark(dev);
   }
   constexpr bool YM = MODE == MODE_YFWD || MODE == MODE_YINV;
   const int NB = (g.M + 1 + K::C - 1) / K::C, W = YM ? g.N3 : g.N2;   // tiles per w, w range

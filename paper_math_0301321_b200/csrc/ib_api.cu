@@ -562,8 +562,11 @@ int ib_step(ib_ctx *c, int32_t nsteps) {
   const long long bad = *c->flag_h;
   c->have_p = c->want_p;
   if (bad != LLONG_MAX) {
-    c->n = bad + 1;
-    return fail(IB_ENONFINITE, "non-finite u or X at step " + std::to_string(bad));
+    // the batch ran to its end on the device (u, X and the device counter are at n0 +
+    // nsteps), so the host counter follows them; the first bad step is in the message
+    c->n = n0 + nsteps;
+    return fail(IB_ENONFINITE, "non-finite u or X first at step " + std::to_string(bad) +
+                                   " (state left at step " + std::to_string(c->n) + ")");
   }
   c->n += nsteps;
   return IB_OK;

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <atomic>
 #include <string>
 #include <vector>
 
@@ -116,6 +117,29 @@ struct ib_ctx {
 };
 
 namespace ibk {
+// Once-per-device host state (function attributes apply to the current device only; a
+// second context on another GPU of the same process must set them again).
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+struct PerDeviceOnce {
+  std::atomic<unsigned long long> bits{0};
+  bool done(int dev) const { return dev < 64 && ((bits.load() >> dev) & 1ull); }
+  void mark(int dev) { if (dev < 64) bits.fetch_or(1ull << dev); }
+};
+// SM count of the current device (cached per device)
+inline int sm_count() {
+  static std::atomic<int> cache[64];
+  const int d = current_device();
+  int v = d < 64 ? cache[d].load() : 0;
+  if (!v) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
+    if (d < 64) cache[d].store(v);
+  }
+  return v;
+}
 // kernels/launchers (fluid.cu)
 cudaError_t init_tables(ib_ctx *c);
 cudaError_t fluid_setup_attributes(int N);

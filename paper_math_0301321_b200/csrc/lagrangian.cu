@@ -341,18 +341,13 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
                                 const long long *dev_n, long long n, double *F,
                                 unsigned *rowflag, cudaStream_t s) {
   if (sd.np > 0) {
-    static int cap[2] = {0, 0};                 // resident blocks on the device (persistent)
-    const int fa = f_in ? 1 : 0;
-    if (!cap[fa]) {
-      int dev = 0, nsm = 0, per = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-      if (f_in) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_force_spread<true>, SPREAD_THREADS, 0);
-      else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_force_spread<false>, SPREAD_THREADS, 0);
-      cap[fa] = nsm * (per > 0 ? per : 1);
-    }
+    // resident blocks on the current device (persistent grid)
+    int per = 0;
+    if (f_in) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_force_spread<true>, SPREAD_THREADS, 0);
+    else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_force_spread<false>, SPREAD_THREADS, 0);
+    const int64_t cap = (int64_t)sm_count() * (per > 0 ? per : 1);
     const int64_t need = (sd.np + SPREAD_THREADS - 1) / SPREAD_THREADS;
-    const unsigned blocks = (unsigned)(need < cap[fa] ? need : cap[fa]);
+    const unsigned blocks = (unsigned)(need < cap ? need : cap);
     if (f_in)
       k_force_spread<true><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag);
     else

@@ -119,6 +119,7 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
   bool bad = false;
   for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G) {
     const int s = i % S;
+    if (s % G != grp) __trap();                          // ring-ownership rule (XT)
     const int z = IBK_XI_REV ? N3 - 1 - (tile >> lgy) : (tile >> lgy), y0 = (tile & (NYB - 1)) * RB;
     double2 *sm = stage0 + (size_t)s * SW;
     // X_e of this row: half e / HC, position e % HC (one half when N <= 256)
@@ -145,6 +146,9 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
     auto sync_after_load = [&]() { named_bar(bar, NTG); };
     double2 *sp = sm + pencil * LD;
     fft_io<M, +1, false, true>(sp, t, twM, ld, st, sync_after_load);
+    // the pencil stores above are generic-proxy writes into the stage the producer refills
+    // with TMA (async proxy): order them before the release
+    fence_proxy_async();
     named_bar(bar, NTG);
     if (gtid == 0) mbar_arrive(&done[s]);
   }
@@ -202,9 +206,8 @@ bool xpass_encode_s1(const FluidGeom &g, const double2 *spec, XMapsS *m) {
 
 template <class Kern>
 static int grid_for(Kern k, int threads, size_t smem, int ntiles) {
-  int dev = 0, nsm = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  int per = 0;
+  const int nsm = sm_count();
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, threads, smem);
   if (per < 1) per = 1;
   return ntiles < per * nsm ? ntiles : per * nsm;
@@ -216,12 +219,13 @@ static cudaError_t xinv_n(const FluidGeom &g, const XMapsS &m, double *out, cons
                           long long n, cudaStream_t s) {
   using K = XT<N>;
   const size_t smem = (size_t)K::SI_STAGES * K::SI + 1024;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr;
+  const int dev = current_device();
+  if (!attr.done(dev)) {
     cudaError_t e = cudaFuncSetAttribute(k_xinv_tma<N>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)smem);
     if (e != cudaSuccess) return e;
-    attr = true;
+    attr.mark(dev);
   }
   const int grid = grid_for(k_xinv_tma<N>, K::NTHR, smem, g.N3 * (g.N2 / K::RB));
   k_xinv_tma<N><<<grid, K::NTHR, smem, s>>>(g, m.main, m.nyq, out, twN, twM, flag, dev_n, n);

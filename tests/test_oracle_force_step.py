@@ -193,3 +193,33 @@ def test_window_fixed_points_still_spread_their_force(olib):
     F = olib.spread(16, cfg.h, cfg.X, f)
     assert np.allclose(F.reshape(3, -1).sum(1) * cfg.h ** 3, f.sum(0), rtol=0,
                        atol=1e-13 * np.abs(f).sum())
+
+
+# ---------------------------------------------------------------- time coupling (eq:discreteX)
+@pytest.mark.parametrize("N,m", [(16, 3), ((16, 32, 8), 5)])
+def test_step_interpolates_new_velocity_at_old_positions(olib, N, m):
+    """Pins the time levels of eq:discreteX (PAPER.md 725-734, lines 729-730): X^{n+1} =
+    X^n + dt sum_x u^{n+1}(x) delta_h(x - X^n) h^3.  Free points (F = 0) in the shear mode
+    u^0 = A sin(2 pi m y) e_x: u^{n+1} = g u^n with the closed-form viscous gain g
+    (tests/closed_forms.py), so X_x^1 - X_x^0 = dt g A S(Y) and X_x^2 - X_x^1 = dt g^2 A S(Y)
+    with S(Y) = sum_b phi(j_b - Y/h) sin(2 pi m j_b/N2).  Interpolating u^n instead of u^{n+1}
+    misses by the factor 1 - g (0.18-0.24 here)."""
+    import closed_forms as cf
+    from gen import decaying_shear_config
+    cfg = decaying_shear_config(N=N, m=m, seed=8)
+    o = olib.Oracle.from_config(cfg)
+    X0 = cfg.X.copy()
+    for n in (1, 2):
+        o.step(1)
+        want, g = cf.shear_positions(cfg, n)
+        assert 0.15 < 1.0 - g < 0.8
+        # the fluid: u^n = g^n u^0 (advection 0, projection inactive)
+        assert np.max(np.abs(o.u - g ** n * cfg.u0)) <= 1e-14 * cfg.info["A"]
+        d_got, d_want = o.X - X0, want - X0
+        assert np.max(np.abs(d_got - d_want)) <= 1e-12 * np.max(np.abs(d_want))
+        assert np.max(np.abs(o.X[:, 1:] - X0[:, 1:])) <= 1e-16
+    # the wrong coupling (u^n at X^n) would have given dt A S(Y) in the first step
+    o1 = olib.Oracle.from_config(cfg)
+    o1.step(1)
+    wrong = cfg.dt * cfg.info["A"] * cf.shear_interp(X0[:, 1], o1.dims[1], cfg.h, m)
+    assert np.max(np.abs((o1.X[:, 0] - X0[:, 0]) - wrong)) > 0.15 * np.max(np.abs(wrong))
