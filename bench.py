@@ -29,6 +29,7 @@ if ROOT not in sys.path:
 
 METRIC = "IB time steps/sec at 256^3 grid (fp64); per-stage achieved HBM GB/s vs peak"
 UNIT = "steps/s"
+SORT_PERIOD = 32          # steps between re-binnings inside ib_step (csrc ib_internal.cuh)
 
 
 # ------------------------------------------------------------------ algorithmic bytes
@@ -69,10 +70,14 @@ def load_peaks() -> dict:
     return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
 
 
-def ncu_traffic(stage: str):
-    """dram__bytes_read.sum + dram__bytes_write.sum per launch for `stage` from the committed
-    ncu --set full summary (profiles/ncu_traffic.json), else None."""
-    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def cfg_key(k) -> str:
+    return f"cfg{k}"
+
+
+def ncu_traffic(stage: str, config) -> float | None:
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `stage` for THIS config from
+    its committed ncu --set full summary (profiles/ncu_traffic_cfg<k>.json), else None."""
+    p = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg_key(config)}.json")
     if not os.path.exists(p):
         return None
     try:
@@ -81,6 +86,27 @@ def ncu_traffic(stage: str):
         return None if v is None else float(v)
     except Exception:
         return None
+
+
+def ncu_source(config) -> str | None:
+    p = os.path.join(ROOT, "profiles", f"ncu_traffic_{cfg_key(config)}.json")
+    if not os.path.exists(p):
+        return None
+    try:
+        return json.load(open(p)).get("source")
+    except Exception:
+        return None
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 # ------------------------------------------------------------------ clocks
@@ -220,7 +246,8 @@ def run_reference(args, ws, rank):
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, args.config),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": oracle.get_threads(),
-                             "kind": "oracle", "sample": sample},
+                             "kind": "oracle", "sample": sample, "cpu_model": cpu_model(),
+                             "host_cpus": os.cpu_count()},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -280,29 +307,57 @@ def run_ours(args, ws, rank, local):
     ms_max = reduce_max(ms)
     value = job_throughput(ws, args.steps, ms_max)
 
-    # per-stage roofline against the measured HBM copy peak
+    # per-stage roofline against the measured HBM copy peak: algorithmic bytes (DESIGN.md §5
+    # model) and, beside them, the ncu-measured DRAM bytes of this config's committed capture
     peaks = load_peaks()
     sb = stage_bytes(N, npts)
     per_stage = {}
     for k, t in stages.items():
         avg = t / args.steps
         gbs = sb[k] / (avg / 1e3) / 1e9 if avg > 0 else None
+        nb = ncu_traffic(k, args.config)
+        dgbs = nb / (avg / 1e3) / 1e9 if (nb is not None and avg > 0) else None
         per_stage[k] = {"ms": avg, "alg_bytes": sb[k], "gbs": gbs,
-                        "frac": gbs / peaks["hbm_gbs"] if gbs else None}
+                        "frac": gbs / peaks["hbm_gbs"] if gbs else None,
+                        "dram_bytes": nb, "dram_gbs": dgbs,
+                        "dram_frac": dgbs / peaks["hbm_gbs"] if dgbs else None}
+    # the re-binning (counting sort of the points by cell) runs every 32 steps outside the
+    # step graph; timed here on its own and reported amortised
+    rb0, rb1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nrb = 5
+    with torch.cuda.stream(stream):
+        ctx.rebin()
+        rb0.record(stream)
+        for _ in range(nrb):
+            ctx.rebin()
+        rb1.record(stream)
+    torch.cuda.synchronize()
+    rebin_ms = rb0.elapsed_time(rb1) / nrb
+    per_stage["rebin_amortized"] = {"ms": rebin_ms / SORT_PERIOD, "ms_per_call": rebin_ms,
+                                    "period_steps": SORT_PERIOD}
     dom = max(stages, key=lambda k: stages[k])
     avg_dom = stages[dom] / args.steps
     achieved = sb[dom] / (avg_dom / 1e3) / 1e9
     step_bytes = sum(sb.values())
+    ms_step = ms_max / args.steps
+    ncu_step = [ncu_traffic(k, args.config) for k in stages]
+    ncu_step_bytes = sum(ncu_step) if all(v is not None for v in ncu_step) else None
+    nb_dom = ncu_traffic(dom, args.config)
     roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peaks["hbm_gbs"],
-            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": ncu_traffic(dom),
+            "unit": "GB/s", "frac": achieved / peaks["hbm_gbs"], "traffic": nb_dom,
+            "dram_frac": (nb_dom / (avg_dom / 1e3) / 1e9 / peaks["hbm_gbs"]) if nb_dom else None,
+            "traffic_source": ncu_source(args.config),
             "peak_source": peaks["source"],
             "timing": "kernel: mean per-stage CUDA-event time over a second timed region of "
                       f"{args.steps} steps (stage events, no graph; {ms_staged / args.steps:.4f} "
                       "ms/step there)",
-            "step": {"alg_bytes": step_bytes, "ms": ms_max / args.steps,
-                     "gbs": step_bytes / (ms_max / args.steps / 1e3) / 1e9,
-                     "frac": step_bytes / (ms_max / args.steps / 1e3) / 1e9 / peaks["hbm_gbs"],
-                     "frac_of_nominal_8tbs": step_bytes / (ms_max / args.steps / 1e3) / 8e12}}
+            "step": {"alg_bytes": step_bytes, "ms": ms_step,
+                     "gbs": step_bytes / (ms_step / 1e3) / 1e9,
+                     "frac": step_bytes / (ms_step / 1e3) / 1e9 / peaks["hbm_gbs"],
+                     "dram_bytes": ncu_step_bytes,
+                     "dram_frac": (ncu_step_bytes / (ms_step / 1e3) / 1e9 / peaks["hbm_gbs"])
+                     if ncu_step_bytes else None,
+                     "ms_incl_rebin": ms_step + rebin_ms / SORT_PERIOD}}
 
     # end-to-end through the C-ABI with pinned host buffers: per step H2D (u, X), step,
     # D2H (u, X)
@@ -340,7 +395,8 @@ def run_ours(args, ws, rank, local):
                 "dtype": "f64", "data": "synthetic", "config": workload_config(cfg, args.config),
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
                 "gpu_launches": launches,
-                "throughput": {"cells_per_s": value * int(np.prod(dims(N))), "points_per_s": value * npts},
+                "throughput": {"cells_per_s": value * int(np.prod(dims(N))), "points_per_s": value * npts,
+                               "steps_per_s_incl_rebin": ws * 1e3 / roof["step"]["ms_incl_rebin"]},
                 "stages": per_stage}
         print(json.dumps(line), flush=True)
     return 0
@@ -348,10 +404,12 @@ def run_ours(args, ws, rank, local):
 
 def cpu_baseline(args):
     """The oracle as it stands, on this host's cores, on a bounded sample: IB steps of the
-    same config until about 10 s of CPU time have passed (at least one step)."""
+    same config until about 10 s have passed (at least one step) on all cores, then one
+    step on a single thread (1 thread is the baseline, all cores beside it)."""
     import oracle
     from gen import make_config
-    oracle.set_threads(os.cpu_count() or 1)
+    ncores = os.cpu_count() or 1
+    oracle.set_threads(ncores)
     cfg = make_config(args.config)
     o = oracle.Oracle.from_config(cfg)
     k, t0 = 0, time.perf_counter()
@@ -359,9 +417,22 @@ def cpu_baseline(args):
         o.step(1)
         k += 1
     dt = time.perf_counter() - t0
+    one = None
+    if not args.no_cpu_1thread:
+        oracle.set_threads(1)
+        k1, t1 = 0, time.perf_counter()
+        while k1 < 1 or (time.perf_counter() - t1 < 5.0 and k1 < 50):
+            o.step(1)
+            k1 += 1
+        d1 = time.perf_counter() - t1
+        one = {"value": k1 / d1, "unit": UNIT, "cores": 1,
+               "sample": f"{k1} full IB step(s) of cfg{args.config}, {d1:.1f} s"}
+        oracle.set_threads(ncores)
     return {"value": k / dt, "unit": UNIT, "cores": oracle.get_threads(), "kind": "oracle",
+            "cpu_model": cpu_model(), "host_cpus": ncores,
             "sample": f"{k} full IB steps of cfg{args.config} ({grid_name(cfg.N)}, {cfg.np_} points), "
-                      f"{dt:.1f} s"}
+                      f"{dt:.1f} s on {ncores} threads",
+            "one_thread": one}
 
 
 def main(argv=None):
@@ -372,6 +443,7 @@ def main(argv=None):
     ap.add_argument("--config", default="4", help="1..5 (BASELINE.json configs) or 4h (half-cube)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-1thread", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--ref-max-steps", type=int, default=6)
     args = ap.parse_args(argv)

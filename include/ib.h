@@ -129,6 +129,10 @@ int ib_step(ib_ctx *ctx, int32_t nsteps);
 int ib_get_fields(ib_ctx *ctx, double *u, double *p);
 /* Copy out X^n ([np][3], unwrapped) — the boundary positions of eq:discreteX (725-734). */
 int ib_get_positions(ib_ctx *ctx, double *X);
+/* Re-bin the points by lattice cell now (asynchronous on the ctx stream).  The binning is a
+ * visiting order for spread and interpolation only (DESIGN.md §5 "cell binning"); ib_step
+ * refreshes it every 32 steps by itself.  Exposed so that its cost can be timed. */
+int ib_rebin(ib_ctx *ctx);
 int64_t ib_get_step(ib_ctx *ctx);
 int ib_set_step(ib_ctx *ctx, int64_t n);
 int64_t ib_num_points(ib_ctx *ctx);

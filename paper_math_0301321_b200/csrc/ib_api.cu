@@ -592,6 +592,14 @@ int ib_get_positions(ib_ctx *c, double *X) {
   return IB_OK;
 }
 
+int ib_rebin(ib_ctx *c) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (c->np == 0) return IB_OK;
+  c->since_bin = -1;
+  CK(ensure_binned(c, c->stream));
+  return IB_OK;
+}
+
 int64_t ib_get_step(ib_ctx *c) { return c ? c->n : -1; }
 int ib_set_step(ib_ctx *c, int64_t n) {
   if (!c) return fail(IB_EINVAL, "ctx is NULL");

@@ -21,7 +21,7 @@ IB_OPT_PRESSURE, IB_OPT_STAGE_TIMING, IB_OPT_GRAPH = 1, 2, 3
 
 EXPORTS = ("ib_create", "ib_create3", "ib_destroy", "ib_set_stream", "ib_set_option", "ib_set_structure",
            "ib_set_positions", "ib_set_velocity", "ib_set_drive", "ib_set_fixed", "ib_step", "ib_get_fields",
-           "ib_get_positions", "ib_get_step", "ib_set_step", "ib_num_points", "ib_stage_times",
+           "ib_get_positions", "ib_rebin", "ib_get_step", "ib_set_step", "ib_num_points", "ib_stage_times",
            "ib_launch_count", "ib_last_error", "ib_debug_force", "ib_debug_spread",
            "ib_debug_interp", "ib_debug_rhs", "ib_debug_fluid", "ib_debug_project",
            "ib_debug_fft", "ib_debug_ifft")
@@ -71,6 +71,7 @@ def load(path: Optional[str] = None):
     L.ib_step.argtypes = [p, i32]
     L.ib_get_fields.argtypes = [p, p, p]
     L.ib_get_positions.argtypes = [p, p]
+    L.ib_rebin.argtypes = [p]
     L.ib_get_step.restype = i64
     L.ib_get_step.argtypes = [p]
     L.ib_set_step.argtypes = [p, i64]
@@ -340,6 +341,10 @@ class IBContext:
 
     def get_positions_into(self, X_out):
         ib_get_positions(self.ctx, X_out)
+
+    def rebin(self):
+        """Re-bin the points by cell now (asynchronous on the context stream)."""
+        _check(load().ib_rebin(self.ctx))
 
     def stage_times(self, reset=False):
         return ib_stage_times(self.ctx, reset)

@@ -220,7 +220,7 @@ def _parity(ibm, olib, cfg, steps=(1, 1, 8), tol=(1e-11, 1e-11, 1e-9), elem=1e-1
         Uo = olib.interp(cfg.N, cfg.h, uo, Xo) if X0.size else np.zeros((0, 3))
         e_U = rel_l2(Ug, Uo) if X0.size else 0.0
         m_U = _max_rel(Ug, Uo, float(np.max(np.abs(Uo)))) if X0.size else 0.0
-        report.append({"step": done, "u": e_u, "u_max": m_u, "X": e_X, "X-X0": e_d,
+        report.append({"cfg": cfg.name, "step": done, "u": e_u, "u_max": m_u, "X": e_X, "X-X0": e_d,
                        "U": e_U, "U_max": m_U})
         assert e_u <= t, (cfg.name, done, "u", e_u)
         assert m_u <= elem, (cfg.name, done, "u element-wise", m_u)
@@ -581,3 +581,31 @@ def test_checkpoint_resume_matches_straight_run(ibm):
         u, _ = r.get_fields()
         X = r.get_positions()
     assert rel_l2(u, u_ref) < 1e-12 and rel_l2(X - cfg.X, X_ref - cfg.X) < 1e-10
+
+
+@pytest.mark.slow
+def test_strip_experiment_observables_match_oracle(ibm, olib):
+    """SURVEY 8(f) row 3 against the oracle: the cfg3 strip driven for 100 steps (period 50,
+    total drive 1e-3 as BASELINE.json configs[2]) on the GPU and on the oracle, the centre-line
+    normal displacement (experiments.centerline) compared station by station every 10 steps
+    (max |d_gpu - d_oracle| <= 1e-9 max |d_oracle|), then the envelopes and their peak."""
+    from paper_math_0301321_b200 import experiments as ex
+    cfg = ex._scaled(make_config(3), 1.0, 50)
+    rows, _ = ex.strip_rows(cfg)
+    s, n = ex.rest_frame(cfg)
+    X0 = cfg.X.copy()
+    o = olib.Oracle.from_config(cfg)
+    pg, po = [], []
+    with ibm.IBContext.from_config(cfg) as c:
+        for _ in range(10):
+            c.step(10)
+            o.step(10)
+            dg = ex.centerline(c.get_positions(), X0, rows, n)
+            do = ex.centerline(o.get_positions(), X0, rows, n)
+            assert np.max(np.abs(dg - do)) <= 1e-9 * np.max(np.abs(do)), c.n
+            pg.append(dg)
+            po.append(do)
+    eg, eo = ex.envelope(pg), ex.envelope(po)
+    assert eo.max() > 0
+    assert np.max(np.abs(eg - eo)) <= 1e-9 * eo.max()
+    assert ex.peak_location(eg, s) == ex.peak_location(eo, s)

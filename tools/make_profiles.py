@@ -1,13 +1,13 @@
 """Turn a gpurun_out/ capture into the committed profiles/ summaries.
 
-  python tools/make_profiles.py <tag>      (reads gpurun_out/{launches,prof,bench}_<tag>.*)
+  python tools/make_profiles.py <tag> [config]   (reads gpurun_out/{launches,prof,bench}_<tag>.*)
 
 Writes profiles/<tag>_launches.txt (per-launch device times from the
 `ncu --metrics gpu__time_duration.sum --clock-control none` pass, with each kernel's share
 of the step), profiles/<tag>_ncu_full.txt (per-kernel `ncu --set full` summary: duration,
 DRAM bytes, L2 hit rate, occupancy, bank conflicts), profiles/<tag>_bench.json (the bench
-line) and profiles/ncu_traffic.json (DRAM bytes per launch per stage, read by bench.py for
-roofline.traffic).
+line) and profiles/ncu_traffic_cfg<config>.json (DRAM bytes per launch per stage of that
+config, read by bench.py for roofline.traffic / dram_frac).
 """
 import csv
 import io
@@ -20,18 +20,24 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
+import re
+
+# kernel name -> stage of the step (any lattice size): the TMA column kernel's MODE is its
+# second template argument (0 = z solve, 1 = y forward, 2 = y inverse, 3/4 = debug z passes)
+_COL = {"0": "z_solve", "1": "y_fwd", "2": "y_inv", "3": "z_fwd", "4": "z_inv"}
 STAGE_OF = [("k_force_spread", "force_spread"), ("k_drive_spread", "force_spread"),
-            ("k_xfwd", "xfwd_rhs_r2c"), ("k_ypass<256, (int)-1>", "y_fwd"),
-            ("k_ypass<(int)256, (int)-1>", "y_fwd"), ("k_ypass<256, 1>", "y_inv"),
-            ("k_ypass<(int)256, (int)1>", "y_inv"), ("k_zpass", "z_solve"),
-            ("k_colfft<256, 1>", "y_fwd"), ("k_colfft<256, 0>", "z_solve"),
-            ("k_colfft<256, 2>", "y_inv"), ("k_colfft<(int)256, (int)1>", "y_fwd"),
-            ("k_colfft<(int)256, (int)0>", "z_solve"), ("k_colfft<(int)256, (int)2>", "y_inv"),
+            ("k_xfwd", "xfwd_rhs_r2c"), ("k_zpass", "z_solve"),
             ("k_xinv", "xinv_c2r"), ("k_interp", "interp_update"), ("k_step_inc", "step_inc"),
             ("k_bin", "binning"), ("k_scan", "binning")]
 
 
 def stage(name):
+    m = re.search(r"k_colfft<(?:\(int\))?\d+, (?:\(int\))?(\d)>", name)
+    if m:
+        return _COL[m.group(1)]
+    m = re.search(r"k_ypass<(?:\(int\))?\d+, (?:\(int\))?(-?1)>", name)
+    if m:
+        return "y_fwd" if m.group(1) == "-1" else "y_inv"
     for key, st in STAGE_OF:
         if key in name:
             return st
@@ -74,6 +80,7 @@ def num(d, k):
 
 def main():
     tag = sys.argv[1]
+    cfg = sys.argv[2] if len(sys.argv) > 2 else "4"
     os.makedirs(PROF, exist_ok=True)
     L = launches(tag)
     if L:
@@ -114,9 +121,10 @@ def main():
             traffic.setdefault(st, 0.0)
             traffic[st] += rb + wb
         open(os.path.join(PROF, f"{tag}_ncu_full.txt"), "w").write("\n".join(lines) + "\n")
-        json.dump({"source": f"profiles/{tag}_ncu_full.txt (ncu --set full, one step of cfg4)",
+        json.dump({"source": f"profiles/{tag}_ncu_full.txt (ncu --set full, one step of cfg{cfg})",
                    "unit": "bytes per launch (dram__bytes_read.sum + dram__bytes_write.sum)",
-                   "stages": traffic}, open(os.path.join(PROF, "ncu_traffic.json"), "w"), indent=1)
+                   "stages": traffic},
+                  open(os.path.join(PROF, f"ncu_traffic_cfg{cfg}.json"), "w"), indent=1)
     b = os.path.join(OUT, f"bench_{tag}.json")
     if os.path.exists(b):
         txt = open(b).read().strip().splitlines()
