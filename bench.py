@@ -402,6 +402,52 @@ def run_ours(args, ws, rank, local):
     return 0
 
 
+def run_slab(args, ws, rank, local):
+    """--mode slab: the z-slab decomposition.  N = 1: P slab contexts on one
+    GPU with device copies in place of the collectives (an emulation: it measures the
+    decomposed kernels plus the copies, not NVLink); N > 1: one slab per GPU, NCCL
+    all-to-all / all-gather between the phases (total work fixed: strong scaling)."""
+    import torch
+    from gen import make_config
+    from paper_math_0301321_b200 import slab as slabmod
+    torch.cuda.set_device(local)
+    cfg = make_config(args.config)
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        if ws == 1:
+            P = args.slab_P
+            run = slabmod.LocalSlabs(cfg, P, stream)
+            par = f"slab{P} emulated on 1 GPU (device copies in place of collectives)"
+        else:
+            P = ws
+            run = slabmod.DistSlab(cfg)
+            stream = run.stream
+            par = f"slab{P} over {ws} GPUs (NCCL all-to-all / all-gather)"
+        run.step(args.warmup)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(local) as clk:
+            e0.record(stream)
+            run.step(args.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        ms = reduce_max(e0.elapsed_time(e1))
+        run.close()
+    value = args.steps / (ms / 1e3)                  # whole-lattice steps per second
+    if rank == 0:
+        wc = workload_config(cfg, args.config)
+        wc["parallelism"] = par
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": wc, "mode": "slab", "slab_P": P, "clocks": clk.summary(),
+                "note": "not the headline: --mode replicas (default) is; see DESIGN.md §10"}
+        print(json.dumps(line), flush=True)
+    return 0
+
+
 def cpu_baseline(args):
     """The oracle as it stands, on this host's cores, on a bounded sample: IB steps of the
     same config until about 10 s have passed (at least one step) on all cores, then one
@@ -442,6 +488,10 @@ def main(argv=None):
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="4", help="1..5 (BASELINE.json configs) or 4h (half-cube)")
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--mode", choices=["replicas", "slab"], default="replicas",
+                    help="replicas (default, the headline): one independent IB run per GPU; "
+                         "slab: the z-slab decomposition of one lattice")
+    ap.add_argument("--slab-P", type=int, default=4, help="slabs emulated on one GPU (--mode slab, N = 1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-1thread", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)
@@ -458,6 +508,8 @@ def main(argv=None):
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
+        if args.mode == "slab":
+            return run_slab(args, ws, rank, local)
         return run_ours(args, ws, rank, local)
     finally:
         if ws > 1:

@@ -147,6 +147,39 @@ int64_t ib_launch_count(ib_ctx *ctx, int32_t reset);
 
 const char *ib_last_error(void);
 
+/* ---- slab decomposition along z ----------
+ * The paper partitions its fluid and material grids over processors (PAPER.md 801-807) and
+ * needs it for the 2x refined model (1238-1245).  Rank `rank` of P owns the lattice planes
+ * z in [rank L, (rank + 1) L), L = N3 / P; positions X are replicated on every rank.  One
+ * step = ib_slab_phase 0, 1, 2, 3, 4 with the caller's exchange between phases (all
+ * asynchronous on the ctx stream; the caller orders its collectives or copies on the same
+ * stream):
+ *   after 0: for each component c: all-to-all of s2[c] ([P dst][Ky][L][Pc] complex) into
+ *            z[c] ([P src][Ky][L][Pc]), Ky = N2 / P, Pc = N1/2 + 2 (equal splits);
+ *   after 1: the reverse all-to-all, z[c] -> s2[c];
+ *   after 2: all-gather of edge_send ([3 planes][3][N2][N1] doubles: last, first, second
+ *            owned plane) into edge_recv ([P][3][3][N2][N1]);
+ *   after 3: all-gather of count_send (1 uint64) into count_recv ([P]) and of pack_send
+ *            ([pack_cap] records (x, y, z, index) of doubles) into pack_recv ([P][pack_cap]).
+ * Every buffer is caller-owned DEVICE memory that must outlive the ctx's use of it;
+ * pack_cap >= np.  Requires N1, N2, N3 powers of two in [64, 512], P a power of two
+ * dividing N2 and N3, L >= 8.  The other calls act on the slab: ib_set_structure,
+ * ib_set_drive, ib_set_fixed, ib_set_positions take the whole (replicated) structure;
+ * ib_set_velocity takes the WHOLE lattice u [3][N3][N2][N1]; ib_get_fields returns the owned
+ * planes [3][L][N2][N1] (no pressure); ib_step and the ib_debug_* calls return IB_ESTATE. */
+ib_ctx *ib_slab_create(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu,
+                       double dt, int32_t P, int32_t rank);
+/* info[0..7] = P, rank, L, Ky, N1, N2, N3, Pc. */
+int ib_slab_info(ib_ctx *ctx, int32_t *info, int32_t cap);
+int ib_slab_set_buffers(ib_ctx *ctx, void *s2, void *z, double *edge_send, double *edge_recv,
+                        void *pack_send, void *pack_recv, uint64_t *count_send,
+                        uint64_t *count_recv, int64_t pack_cap);
+/* Enqueue phase 0..4 of the next step (see above); phase 4 advances ib_get_step. */
+int ib_slab_phase(ib_ctx *ctx, int32_t phase);
+/* Synchronise the ctx stream; IB_ENONFINITE (first bad step in ib_last_error) if u or X of
+ * this rank became non-finite since the last call. */
+int ib_slab_sync(ib_ctx *ctx);
+
 /* ---- test-only entry points (same library; not part of the product contract) ----------
  * Each runs ONE stage of the step on the given inputs with the same kernels ib_step uses. */
 int ib_debug_force(ib_ctx *ctx, double *f_out);                         /* [np][3], step n  */

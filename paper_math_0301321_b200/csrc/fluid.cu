@@ -76,6 +76,11 @@ __global__ void k_init_tables(double2 *twN, int N, double2 *twM, int M, double *
   }
 }
 
+cudaError_t init_axis_table(double2 *twN, int N, double *s, double *l, double h, cudaStream_t st) {
+  k_init_tables<<<(N + 127) / 128, 128, 0, st>>>(twN, N, nullptr, 0, s, l, h);
+  return cudaGetLastError();
+}
+
 cudaError_t init_tables(ib_ctx *c) {
   const int L[3] = {c->g.N1, c->g.N2, c->g.N3};
   for (int a = 0; a < 3; ++a) {
@@ -115,6 +120,9 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   double *ut = reinterpret_cast<double *>(sm);     // u tile [comp][UR][N1]
   const int N2 = g.N2, N3 = g.N3;                  // rows per plane, planes
   const int z = blockIdx.y, y0 = blockIdx.x * RB;
+  // u array: uN3 planes, local plane z at uz0 + z (slab: ghost planes around the owned ones)
+  const int uN3 = g.uN3, zu = g.uz0 + z;
+  const size_t Vu = (size_t)N * N2 * uN3;
   const int t = threadIdx.x % T, pencil = threadIdx.x / T;
   const int row = pencil % RB, comp = pencil / RB, y = y0 + row;
   const size_t V = (size_t)g.V;
@@ -126,7 +134,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
       fence_mbar_init();
       mbar_expect_tx(&tbar, (uint32_t)(3 * UR * N * 8));
       for (int c = 0; c < 3; ++c) {
-        const int rb = (c * N3 + z) * N2;
+        const int rb = (c * uN3 + zu) * N2;
         tma_load_2d(ut + ((size_t)c * UR + 1) * N, &map_rows, 0, rb + y0, &tbar);
         tma_load_2d(ut + (size_t)c * UR * N, &map_row1, 0, rb + ((y0 - 1 + N2) & (N2 - 1)), &tbar);
         tma_load_2d(ut + ((size_t)c * UR + RB + 1) * N, &map_row1, 0, rb + ((y0 + RB) & (N2 - 1)), &tbar);
@@ -140,7 +148,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
       const int ch = idx % CH, rr = (idx / CH) % UR, cc = idx / (CH * UR);
       const int yy = (y0 - 1 + rr + N2) & (N2 - 1);
       cp_async16(ut + ((size_t)cc * UR + rr) * N + 2 * ch,
-                 u + cc * V + ((size_t)z * N2 + yy) * N + 2 * ch, true);
+                 u + cc * Vu + ((size_t)zu * N2 + yy) * N + 2 * ch, true);
     }
     cp_async_commit();
     cp_async_wait_all();
@@ -148,9 +156,12 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   }
   // F is only read on rows the spread touched (row flags), else taken as 0
   const bool hasF = MODE == 1 || (MODE == 0 && (rowflag == nullptr || rowflag[(size_t)z * N2 + y] != 0));
-  const size_t zm = ((size_t)((z + N3 - 1) & (N3 - 1)) * N2 + y) * N;
-  const size_t zp = ((size_t)((z + 1) & (N3 - 1)) * N2 + y) * N;
-  const double *uc_ = u + (MODE == 2 ? 0 : comp * V);
+  // z -+ 1: periodic on the whole lattice; in a slab the neighbours are ghost planes
+  const int zmi = g.slab ? zu - 1 : ((z + N3 - 1) & (N3 - 1));
+  const int zpi = g.slab ? zu + 1 : ((z + 1) & (N3 - 1));
+  const size_t zm = ((size_t)zmi * N2 + y) * N;
+  const size_t zp = ((size_t)zpi * N2 + y) * N;
+  const double *uc_ = u + (MODE == 2 ? 0 : comp * Vu);
   const double *own = ut + ((size_t)comp * UR + row + 1) * N;        // this row, own comp
 
   // r at the cell pair (2e, 2e+1) of this thread's component: sum_k u_k D_k^{+-} u_i
@@ -162,8 +173,17 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
     const double2 v1 = *reinterpret_cast<const double2 *>(ut + (1 * UR + row + 1) * N + x);
     const double2 v2 = *reinterpret_cast<const double2 *>(ut + (2 * UR + row + 1) * N + x);
     const double2 c = comp == 0 ? v0 : (comp == 1 ? v1 : v2);
-    const double xm = own[(x + N - 1) & (N - 1)];
-    const double xp = own[(x + 2) & (N - 1)];
+#ifndef IBK_XSWAP
+#define IBK_XSWAP 1
+#endif
+    // x neighbours (8-byte loads, served per half-warp = two rows of one component): odd
+    // rows fetch them in the opposite order, so the two rows of a half-warp hit the
+    // disjoint bank halves of x - 1 and x + 2 instead of the same one (2-way conflict)
+    const int ixm = (x + N - 1) & (N - 1), ixp = (x + 2) & (N - 1);
+    const bool sw = IBK_XSWAP && (row & 1);
+    const double l0 = own[sw ? ixp : ixm];
+    const double l1 = own[sw ? ixm : ixp];
+    const double xm = sw ? l1 : l0, xp = sw ? l0 : l1;
     const double2 a_ym = *reinterpret_cast<const double2 *>(own - N + x);
     const double2 a_yp = *reinterpret_cast<const double2 *>(own + N + x);
     const double2 a_zm = __ldg(reinterpret_cast<const double2 *>(uc_ + zm + x));
@@ -558,7 +578,7 @@ bool xfwd_encode_u(const FluidGeom &g, const double *u, XMapsU *m) {
     case 128: rb = XCfg<128>::RB; break;  case 256: rb = XCfg<256>::RB; break;
     default: return false;
   }
-  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)3 * g.N2 * g.N3}, strides[1] = {(cuuint64_t)N * 8};
+  cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)3 * g.N2 * g.uN3}, strides[1] = {(cuuint64_t)N * 8};
   cuuint32_t box[2] = {(cuuint32_t)N, (cuuint32_t)rb}, box1[2] = {(cuuint32_t)N, 1u}, es[2] = {1, 1};
   void *base = const_cast<double *>(u);
   if (fn(&m->rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,

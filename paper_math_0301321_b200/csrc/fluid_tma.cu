@@ -211,6 +211,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
 
   // 2-D maps address rows (comp*N + w)*N + r; 3-D maps (x, w, comp*N + r) — see encode()
   constexpr bool LD3 = MODE == MODE_YINV, ST3 = MODE == MODE_YFWD;
+  constexpr bool SLABZ = MODE == MODE_Z;                 // slab z pass: 5-D maps
   if (threadIdx.x >= NT) {                               // ---------------- producer warp
     if (threadIdx.x == NT) {
       prefetch_tmap(&map_ld);
@@ -224,6 +225,8 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
           for (int r0 = 0; r0 < N; r0 += BR) {
             double2 *d = b + c * K::TILE + r0 * C;
             if (LD3) tma_load_3d(d, &map_ld, x, w, (c0 + c) * N + r0, &full[s]);
+            else if (SLABZ && g.slab)   // received slab blocks [comp][src][ky][z_src][kx]
+              tma_load_5d(d, &map_ld, x, 0, w, r0 / g.L, c0 + c, &full[s]);
             else     tma_load_2d(d, &map_ld, x, ((c0 + c) * W + w) * N + r0, &full[s]);
           }
       };
@@ -234,6 +237,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
           for (int r0 = 0; r0 < N; r0 += BR) {
             const double2 *d = b + c * K::TILE + r0 * C;
             if (ST3) tma_store_3d(&map_st, x, w, (c0 + c) * N + r0, d);
+            else if (SLABZ && g.slab) tma_store_5d(&map_st, x, 0, w, r0 / g.L, c0 + c, d);
             else     tma_store_2d(&map_st, x, ((c0 + c) * W + w) * N + r0, d);
           }
         bulk_commit();
@@ -267,24 +271,35 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   const int col = gtid % C, t = (gtid / C) % T, comp = gtid / (C * T);
   int i = grp;
   Walk cw(blockIdx.x + grp * gridDim.x, G * gridDim.x, NB, WW);
-  const double cdt = g.rho / g.dt, invV = 1.0 / (double)g.V;   // solve constants (MODE_Z)
+  const double cdt = g.rho / g.dt, invV = 1.0 / (double)g.Vg;  // solve constants (MODE_Z)
   for (int tile = blockIdx.x + grp * gridDim.x; tile < ntiles; tile += G * gridDim.x, i += G, cw.next()) {
     const int s = i % S;
     if (s % G != grp) __trap();                          // ring-ownership rule (ColCfg)
+    // MODE_Z: the tile's x / y symbols are read before the stage wait and the forward FFT,
+    // so their L1/L2 latency overlaps them instead of stalling the solve
+    const int kx0 = C * cw.x, ky = cw.w;
+    const int kyg = g.ky0 + ky;                          // global ky (slab z pass: offset)
+    static_assert(NTG % C == 0, "solve mapping");
+    const int c = gtid % C, kx = kx0 + c;                // column c = gtid % C per thread
+    const bool live = kx <= M;
+    double sy = 0.0, ly = 0.0, sx = 0.0, lx = 0.0;
+    auto load_sym = [&]() {
+      sy = sym.sy[kyg]; ly = sym.ly[kyg];
+      if (live) { sx = sym.sx[kx]; lx = sym.lx[kx]; }
+    };
+#ifndef IBK_ZHOIST
+#define IBK_ZHOIST 1
+#endif
+    if (MODE == MODE_Z && IBK_ZHOIST) load_sym();
     mbar_wait(&full[s], (i / S) & 1);
     double2 *buf = stage0 + (size_t)s * NC * K::TILE;
     double2 *pc = buf + comp * K::TILE;
     auto A = [pc, col](int e) -> double2 & { return pc[swz<C>(e, col)]; };
     if (MODE == MODE_Z) {
       fft_inplace<N, -1, C>(A, t, tw, bar, NTG);
-      const int kx0 = C * cw.x, ky = cw.w;               // NC = 3 here
-      const double sy = sym.sy[ky], ly = sym.ly[ky];
-      const bool ny = (ky == 0) || (2 * ky == g.N2);
-      // column c = gtid % C is fixed per thread (NTG is a multiple of C): x symbols once
-      static_assert(NTG % C == 0, "solve mapping");
-      const int c = gtid % C, kx = kx0 + c;
-      const bool live = kx <= M;
-      const double sx = live ? sym.sx[kx] : 0.0, lxy = (live ? sym.lx[kx] : 0.0) + ly;
+      if (!IBK_ZHOIST) load_sym();
+      const bool ny = (kyg == 0) || (2 * kyg == g.N2g);
+      const double lxy = lx + ly;
       const bool nxy = ny && (kx == 0 || kx == M);
       // û = (r̂ - s (s.r̂)/|s|^2)/d, p̂ = -i (s.r̂)/|s|^2; null modes (Z6): û = r̂/d
       auto solve = [&](int kz, double2 *q0, double2 r0, double2 r1, double2 r2) {
@@ -373,6 +388,26 @@ static bool encode(CUtensorMap *m, void *base, int rank, const FluidGeom &g, int
 }
 
 static int zcols(int N3) { return N3 >= 128 ? 4 : 8; }   // = ColCfg<N3, MODE_Z>::C
+
+// Slab z pass: the received transpose blocks Z [comp][src][ky][z_src][kx]
+// (P source ranks of L planes each, Ky local ky rows, pitch gz.P complex) as a 5-D map
+// (x, z_src, ky, src, comp); a box {2C, L, 1, BR/L, 1} is BR consecutive rows kz = src L + z.
+bool colfft_encode_slabz(const FluidGeom &gz, double2 *Z, int P, CUtensorMap *m) {
+  auto fn = encode_fn();
+  const int N = gz.N3, L = gz.L, C = zcols(N);
+  const int br = N < 256 ? N : 256;
+  if (!fn || !colfft_supported(N) || L * P != N || br % L) return false;
+  const cuuint64_t row = (cuuint64_t)gz.P * 16;
+  cuuint64_t dims[5] = {(cuuint64_t)2 * (gz.M + 1), (cuuint64_t)L, (cuuint64_t)gz.N2,
+                        (cuuint64_t)P, 3};
+  cuuint64_t strides[4] = {row, row * L, row * L * gz.N2, row * L * gz.N2 * P};
+  cuuint32_t box[5] = {(cuuint32_t)(2 * C), (cuuint32_t)L, 1, (cuuint32_t)(br / L), 1};
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, Z, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            C == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 bool colfft_supported(int N) { return N >= 64 && N <= 512; }
 

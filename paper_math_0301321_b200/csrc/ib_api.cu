@@ -15,51 +15,17 @@
 #include <string>
 #include <vector>
 
-#include "ib_internal.cuh"
+#include "api.cuh"
 
 using namespace ibk;
 
 static thread_local std::string g_err;
 
-static int fail(int code, const std::string &msg) {
+namespace ibk {
+
+int fail(int code, const std::string &msg) {
   g_err = msg;
   return code;
-}
-
-#define CK(expr)                                                                    \
-  do {                                                                              \
-    cudaError_t e_ = (expr);                                                        \
-    if (e_ != cudaSuccess)                                                          \
-      return fail(e_ == cudaErrorMemoryAllocation ? IB_ENOMEM : IB_ECUDA,           \
-                  std::string(#expr) + ": " + cudaGetErrorString(e_));             \
-  } while (0)
-
-namespace {
-
-template <class T>
-cudaError_t dalloc(T **p, size_t count) {
-  return cudaMalloc((void **)p, count * sizeof(T) > 0 ? count * sizeof(T) : 1);
-}
-
-void dfree(void *p) {
-  if (p) cudaFree(p);
-}
-
-// Copy count elements from a host-or-device pointer to a host vector.
-template <class T>
-cudaError_t to_host(std::vector<T> &dst, const T *src, size_t count, cudaStream_t s) {
-  dst.resize(count);
-  if (!count) return cudaSuccess;
-  cudaError_t e = cudaMemcpyAsync(dst.data(), src, count * sizeof(T), cudaMemcpyDefault, s);
-  if (e != cudaSuccess) return e;
-  return cudaStreamSynchronize(s);
-}
-
-cudaError_t copy_sync(void *dst, const void *src, size_t bytes, cudaStream_t s) {
-  if (!bytes) return cudaSuccess;
-  cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
-  if (e != cudaSuccess) return e;
-  return cudaStreamSynchronize(s);
 }
 
 __global__ void k_count_nonfinite(const double *a, size_t n, unsigned long long *cnt) {
@@ -226,7 +192,7 @@ struct Tmp {
   }
 };
 
-}  // namespace
+}  // namespace ibk
 
 extern "C" {
 
@@ -261,6 +227,7 @@ ib_ctx *ib_create3(int32_t N1, int32_t N2, int32_t N3, double h, double rho, dou
   c->g.M = N1 / 2; c->g.P = N1 / 2 + 2;
   c->g.V = (int64_t)N1 * N2 * N3;
   c->g.h = h; c->g.invh = 1.0 / h; c->g.rho = rho; c->g.mu = mu; c->g.dt = dt;
+  geom_whole(c->g);
   auto bad = [&](cudaError_t e, const char *what) {
     fail(e == cudaErrorMemoryAllocation ? IB_ENOMEM : IB_ECUDA,
          std::string("ib_create: ") + what + ": " + cudaGetErrorString(e));
@@ -343,6 +310,7 @@ int ib_set_option(ib_ctx *c, int32_t opt, int64_t value) {
   if (!c) return fail(IB_EINVAL, "ctx is NULL");
   switch (opt) {
     case IB_OPT_PRESSURE:
+      if (c->slab_P && value) return fail(IB_ESTATE, "slab context: no pressure output");
       c->want_p = value != 0;
       if (c->want_p && !c->pspec) {
         CK(dalloc(&c->pspec, pspec_elems(c)));
@@ -421,8 +389,8 @@ int ib_set_structure(ib_ctx *c, const double *points, int64_t np, const ib_patch
   CK(dalloc(&c->X, (size_t)np * 3));
   CK(dalloc(&c->perm, (size_t)np));
   if (np > 0 && !c->bincnt) {
-    CK(dalloc(&c->bincnt, (size_t)c->g.V));
-    CK(dalloc(&c->binsum, (size_t)bin_scan_blocks(c->g.V)));
+    CK(dalloc(&c->bincnt, (size_t)c->g.Vg));            // cells of the whole lattice
+    CK(dalloc(&c->binsum, (size_t)bin_scan_blocks(c->g.Vg)));
   }
   CK(dalloc(&c->patches, (size_t)npatch));
   CK(dalloc(&c->stiff, (size_t)nstiff));
@@ -453,9 +421,25 @@ int ib_set_positions(ib_ctx *c, const double *points) {
 int ib_set_velocity(ib_ctx *c, const double *u) {
   if (!c) return fail(IB_EINVAL, "ctx is NULL");
   if (!u) return fail(IB_EINVAL, "u is NULL");
-  CK(copy_sync(c->u, u, (size_t)3 * c->g.V * sizeof(double), c->stream));
+  size_t nu = (size_t)3 * c->g.V;
+  if (c->slab_P) {
+    // slab: u is the WHOLE lattice [3][N3][N2][N1]; this rank keeps its planes and ghosts
+    // (global planes z0 - 1 .. z0 + L + 1, periodic)
+    const FluidGeom &g = c->g;
+    const size_t plane = (size_t)g.N1 * g.N2, Vu = plane * g.uN3;
+    for (int comp = 0; comp < 3; ++comp)
+      for (int p = 0; p < g.uN3; ++p) {
+        const int zg = ((g.z0 - g.uz0 + p) % g.N3g + g.N3g) % g.N3g;
+        CK(cudaMemcpyAsync(c->u + comp * Vu + p * plane, u + comp * (size_t)g.Vg + zg * plane,
+                           plane * sizeof(double), cudaMemcpyDefault, c->stream));
+      }
+    CK(cudaStreamSynchronize(c->stream));
+    nu = 3 * Vu;
+  } else {
+    CK(copy_sync(c->u, u, nu * sizeof(double), c->stream));
+  }
   unsigned long long bad = 0;
-  int rc = count_nonfinite(c, c->u, (size_t)3 * c->g.V, &bad);
+  int rc = count_nonfinite(c, c->u, nu, &bad);
   if (rc) return rc;
   if (bad) return fail(IB_EINVAL, "non-finite velocity");
   c->have_p = false;
@@ -521,6 +505,7 @@ int ib_set_fixed(ib_ctx *c, const uint8_t *mask) {
 
 int ib_step(ib_ctx *c, int32_t nsteps) {
   if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (c->slab_P) return fail(IB_ESTATE, "slab context: step with ib_slab_phase 0..4");
   if (nsteps < 0) return fail(IB_EINVAL, "nsteps < 0");
   if (nsteps == 0) return IB_OK;
   cudaStream_t s = c->stream;
@@ -574,6 +559,18 @@ int ib_step(ib_ctx *c, int32_t nsteps) {
 
 int ib_get_fields(ib_ctx *c, double *u, double *p) {
   if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (c->slab_P) {            // slab: the owned planes [3][L][N2][N1]; no pressure
+    if (p) return fail(IB_ESTATE, "slab context: no pressure output");
+    if (u) {
+      const FluidGeom &g = c->g;
+      const size_t plane = (size_t)g.N1 * g.N2, Vu = plane * g.uN3;
+      for (int comp = 0; comp < 3; ++comp)
+        CK(cudaMemcpyAsync(u + comp * (size_t)g.V, c->u + comp * Vu + g.uz0 * plane,
+                           (size_t)g.V * sizeof(double), cudaMemcpyDefault, c->stream));
+      CK(cudaStreamSynchronize(c->stream));
+    }
+    return IB_OK;
+  }
   if (u) CK(copy_sync(u, c->u, (size_t)3 * c->g.V * sizeof(double), c->stream));
   if (p) {
     if (!c->have_p || !c->pspec) return fail(IB_ESTATE, "pressure not available: enable IB_OPT_PRESSURE before ib_step");
@@ -605,6 +602,10 @@ int ib_set_step(ib_ctx *c, int64_t n) {
   if (!c) return fail(IB_EINVAL, "ctx is NULL");
   if (n < 0) return fail(IB_EINVAL, "n < 0");
   c->n = n;
+  if (c->slab_P) {            // slab phases read the device counter directly
+    const long long v = n;
+    CK(copy_sync(c->dev_n, &v, sizeof(v), c->stream));
+  }
   return IB_OK;
 }
 int64_t ib_num_points(ib_ctx *c) { return c ? c->np : -1; }
@@ -639,6 +640,7 @@ int64_t ib_launch_count(ib_ctx *c, int32_t reset) {
 // ------------------------------------------------------------------ debug entry points
 
 int ib_debug_force(ib_ctx *c, double *f_out) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !f_out) return fail(IB_EINVAL, "NULL argument");
   if (c->np == 0) return IB_OK;
   Tmp t; double *f;
@@ -649,6 +651,7 @@ int ib_debug_force(ib_ctx *c, double *f_out) {
 }
 
 int ib_debug_spread(ib_ctx *c, const double *f_node, double *F_out) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !f_node || !F_out) return fail(IB_EINVAL, "NULL argument");
   Tmp t; double *f, *F;
   const size_t V = (size_t)c->g.V;
@@ -665,6 +668,7 @@ int ib_debug_spread(ib_ctx *c, const double *f_node, double *F_out) {
 }
 
 int ib_debug_interp(ib_ctx *c, const double *u, double *U_out) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !u || !U_out) return fail(IB_EINVAL, "NULL argument");
   if (c->np == 0) return IB_OK;
   Tmp t; double *ud, *U;
@@ -679,6 +683,7 @@ int ib_debug_interp(ib_ctx *c, const double *u, double *U_out) {
 }
 
 int ib_debug_rhs(ib_ctx *c, const double *u, const double *F, double *r_out) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !u || !F || !r_out) return fail(IB_EINVAL, "NULL argument");
   Tmp t; double *ud, *Fd, *r;
   const size_t V = (size_t)c->g.V;
@@ -691,6 +696,7 @@ int ib_debug_rhs(ib_ctx *c, const double *u, const double *F, double *r_out) {
 }
 
 int ib_debug_fluid(ib_ctx *c, const double *u, const double *F, double *u_out, double *p_out) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !u || !F || !u_out) return fail(IB_EINVAL, "NULL argument");
   Tmp t; double *ud, *Fd, *pd = nullptr; double2 *ps = nullptr, *ps1 = nullptr;
   const FluidGeom &g = c->g;
@@ -729,6 +735,7 @@ __global__ void k_scale(double *a, size_t n, double f) {
 // unnormalised transforms and of the solve's folded 1/V are undone.  Needs the TMA z pass
 // (N3 in [64, 512]).
 int ib_debug_project(ib_ctx *c, const double *rhat, double *uhat, double *phat) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !rhat || !uhat) return fail(IB_EINVAL, "NULL argument");
   if (!c->maps.z_ok) return fail(IB_ESTATE, "ib_debug_project needs N3 in [64, 512]");
   const FluidGeom &g = c->g;
@@ -770,6 +777,7 @@ int ib_debug_project(ib_ctx *c, const double *rhat, double *uhat, double *phat) 
 // i.e. sum_k X_k e^{+2 pi i sum k_a j_a / N_a} over the full Hermitian spectrum.  The TMA
 // column passes transform 3 component slots; slot 0 carries the data.
 int ib_debug_ifft(ib_ctx *c, const double *in, double *out) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !in || !out) return fail(IB_EINVAL, "NULL argument");
   const FluidGeom &g = c->g;
   cudaStream_t s = c->stream;
@@ -794,6 +802,7 @@ int ib_debug_ifft(ib_ctx *c, const double *in, double *out) {
 }
 
 int ib_debug_fft(ib_ctx *c, const double *in, double *out) {
+  if (c && c->slab_P) return fail(IB_ESTATE, "debug entry points need a whole-lattice context");
   if (!c || !in || !out) return fail(IB_EINVAL, "NULL argument");
   Tmp t; double *ind;
   const FluidGeom &g = c->g;

@@ -35,7 +35,22 @@ struct FluidGeom {
   int M, P;                   // M = N1/2; P = spectrum row pitch in complex (>= M+1)
   int64_t V;                  // N1 N2 N3
   double h, invh, rho, mu, dt;
+  // Slab decomposition along z.  Unless slab != 0 these are
+  // the identity: N2g = N2, N3g = N3, Vg = V, z0 = ky0 = uz0 = 0, uN3 = N3.  In a slab the
+  // arrays above are LOCAL: N3 = L planes (x and y passes) or N2 = Ky rows (z pass).
+  int N2g, N3g;               // global lattice extents along y and z
+  int64_t Vg;                 // global cell count (the 1/V of the unnormalised inverse FFT)
+  int z0;                     // global plane of local plane 0
+  int ky0;                    // z pass: global ky of local row 0
+  int uz0, uN3;               // velocity array: plane index of local plane 0; planes held
+  int L;                      // planes per slab (z pass: the source-rank blocks of a pencil)
+  int slab;                   // 1: no periodic wrap along z inside the local arrays
 };
+// Identity slab fields of a whole-lattice geometry.
+inline void geom_whole(FluidGeom &g) {
+  g.N2g = g.N2; g.N3g = g.N3; g.Vg = g.V;
+  g.z0 = 0; g.ky0 = 0; g.uz0 = 0; g.uN3 = g.N3; g.L = g.N3; g.slab = 0;
+}
 
 // Per-axis symbols (D0 symbol s, -symbol of D+D- l) of the three lattice axes.
 struct Sym {
@@ -114,6 +129,17 @@ struct ib_ctx {
   cudaGraphExec_t graph = nullptr;
   long long graph_key = -1;
   long long *dev_n = nullptr;   // device step counter (drive phase, non-finite flag)
+  // slab decomposition along z (ib_slab_create): rank slab_rank of slab_P.
+  // g then describes the local planes (x and y passes, spread, interp), gz the z pass over
+  // the received transpose blocks; the exchange buffers belong to the caller.
+  int slab_P = 0, slab_rank = 0;
+  ibk::FluidGeom gz{};
+  ibk::TmaMaps zmaps;
+  double2 *s2_ext = nullptr, *z_ext = nullptr;   // [3][N2][L][P] / [3][P][Ky][L][P] complex
+  double *edge_send = nullptr, *edge_recv = nullptr;
+  double4 *pack_send = nullptr, *pack_recv = nullptr;
+  unsigned long long *count_send = nullptr, *count_recv = nullptr;
+  int64_t pack_cap = 0;
 };
 
 namespace ibk {
@@ -142,6 +168,8 @@ inline int sm_count() {
 }
 // kernels/launchers (fluid.cu)
 cudaError_t init_tables(ib_ctx *c);
+// twiddles and symbols of one lattice axis of length N (slab contexts: the whole z axis)
+cudaError_t init_axis_table(double2 *twN, int N, double *s, double *l, double h, cudaStream_t st);
 cudaError_t fluid_setup_attributes(int N);
 // x pass: mode 0 = step (r from u,F; zero F), 1 = r only (write r_out), 2 = FFT of in (1 comp)
 // rowflag (may be null = read all of F): per (z,y) row, set by the spread where F != 0
@@ -167,6 +195,7 @@ cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, in
 // only on S2, 4 = z inverse only on S2 (uses maps.s2_2d)
 bool colfft_supported(int N);
 bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m);
+bool colfft_encode_slabz(const FluidGeom &gz, double2 *Z, int P, CUtensorMap *m);
 cudaError_t colfft_make_maps(const FluidGeom &g, double2 *spec, double2 *spec2, TmaMaps *m);
 // twN: twiddles of the pencil axis (y for modes 1-2, z for 0, 3, 4)
 cudaError_t launch_colfft(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
@@ -184,9 +213,12 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g,
                                 const double *f_in, const long long *dev_n, long long n,
                                 double *F, unsigned *rowflag, cudaStream_t s);
 // fixed (may be null): points with fixed[i] != 0 are not moved
+// pack (slab, may be null): the owned points' X^{n+1} as (x, y, z, index) records, counted
+// in *pack_count
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
-                          const int *perm, const uint8_t *fixed, cudaStream_t s);
+                          const int *perm, const uint8_t *fixed, cudaStream_t s,
+                          double4 *pack = nullptr, unsigned long long *pack_count = nullptr);
 // cell binning: perm = point indices grouped by base cell (5 launches + 1 memset)
 cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
                        unsigned *bsum, int *perm, cudaStream_t s);

@@ -187,7 +187,8 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
   const int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (d >= sd.nd) return;
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const int N1 = g.N1, N2 = g.N2, N3g = g.N3g;
+  const unsigned L = (unsigned)g.N3;           // local planes (all N3 unless a slab)
   const size_t V = (size_t)g.V;
   const double a = drive_factor(sd, dev_n ? *dev_n : n) * g.invh * g.invh * g.invh;
   if (a == 0.0) return;
@@ -202,7 +203,8 @@ __global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n
   const size_t x = (jx + e) & (N1 - 1), y = (jy + b) & (N2 - 1);
 #pragma unroll
   for (int h = 0; h < 2; ++h) {
-    const size_t z = (jz + c0 + 2 * h) & (N3 - 1);
+    const size_t z = (unsigned)(jz + c0 + 2 * h - g.z0) & (unsigned)(N3g - 1);   // local plane
+    if (z >= L) continue;                      // slab: another rank's plane
     const size_t cell = (z * N2 + y) * N1 + x;
     const double w = a * wx[e] * wy[b] * wz[c0 + 2 * h];
     for (int k = 0; k < 3; ++k) atomicAdd(&F[k * V + cell], w * dir[k]);
@@ -244,7 +246,8 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
   if (lane < REC) rec[warp][32][lane] = 0.0;   // (REC <= 32)
   __syncthreads();
   const ib_patch *pt = small ? ptab : sd.patches;
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
+  const int N1 = g.N1, N2 = g.N2, N3g = g.N3g;
+  const unsigned L = (unsigned)g.N3;                     // local planes (all N3 unless a slab)
   const size_t V = (size_t)g.V;
   const int lg1 = __ffs(N1) - 1, lg2 = __ffs(N2) - 1;   // powers of two: no division below
   const double ih3 = g.invh * g.invh * g.invh;
@@ -276,7 +279,7 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
       double wx[4], wy[4], wz[4];
       const int jx = axis_weights(xyz[0], g.invh, wx) & (N1 - 1);
       const int jy = axis_weights(xyz[1], g.invh, wy) & (N2 - 1);
-      const int jz = axis_weights(xyz[2], g.invh, wz) & (N3 - 1);
+      const int jz = axis_weights(xyz[2], g.invh, wz) & (N3g - 1);
       double2 *rw = reinterpret_cast<double2 *>(r);
 #pragma unroll
       for (int bb = 0; bb < 4; ++bb) {
@@ -316,14 +319,16 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
       }
       const unsigned jx = kl & (N1 - 1), jy = (kl >> lg1) & (N2 - 1), jz = kl >> (lg1 + lg2);
       const size_t x = (jx + a) & (N1 - 1), y = (jy + b) & (N2 - 1);
-      const size_t z0 = (jz + c0) & (N3 - 1), z1 = (jz + c0 + 2) & (N3 - 1);
+      // local planes (slab: relative to its first plane; other ranks' planes are skipped)
+      const size_t z0 = (jz + c0 - g.z0) & (N3g - 1), z1 = (jz + c0 + 2 - g.z0) & (N3g - 1);
       const size_t e0 = (z0 * N2 + y) * N1 + x, e1 = (z1 * N2 + y) * N1 + x;
-      atomicAdd(&F[e0], acc[0]);          atomicAdd(&F[e1], acc[1]);
-      atomicAdd(&F[V + e0], acc[2]);      atomicAdd(&F[V + e1], acc[3]);
-      atomicAdd(&F[2 * V + e0], acc[4]);  atomicAdd(&F[2 * V + e1], acc[5]);
-      if (rowflag && a == 0) {                  // mark rows (y, z0), (y, z1) of F non-zero
-        rowflag[z0 * N2 + y] = 1u;
-        rowflag[z1 * N2 + y] = 1u;
+      if (z0 < L) {
+        atomicAdd(&F[e0], acc[0]); atomicAdd(&F[V + e0], acc[2]); atomicAdd(&F[2 * V + e0], acc[4]);
+        if (rowflag && a == 0) rowflag[z0 * N2 + y] = 1u;   // row (y, z0) of F is non-zero
+      }
+      if (z1 < L) {
+        atomicAdd(&F[e1], acc[1]); atomicAdd(&F[V + e1], acc[3]); atomicAdd(&F[2 * V + e1], acc[5]);
+        if (rowflag && a == 0) rowflag[z1 * N2 + y] = 1u;
       }
     }
     __syncwarp();                               // records reused by the next block of points
@@ -362,17 +367,26 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
 // U = sum_c wz_c sum_b wy_b (sum_a wx_a u(jx+a, jy+b, jz+c)) straight from global memory
 // (row sums first, 32-bit cell offsets; a row with no periodic wrap in x is 4 consecutive
 // doubles off one base pointer).  Used by warps whose points span more than IMMA_MAXG boxes.
-__device__ __forceinline__ void interp_direct(const double *__restrict__ u, int N1, int N2,
-                                              int N3, int Vi,
+// Plane of the velocity array holding lattice plane jz + c (jz = floor(Z/h) - 1): periodic on
+// the whole lattice; in a slab the owned point's window jz .. jz + 3 lies in
+// the local planes plus ghosts, local plane of global z at uz0 + (z - z0).
+__device__ __forceinline__ int u_plane(const FluidGeom &g, int jz, int c) {
+  if (!g.slab) return (jz + c) & (g.N3 - 1);
+  return g.uz0 - 1 + (int)((unsigned)(jz + 1 - g.z0) & (unsigned)(g.N3g - 1)) + c;
+}
+
+__device__ __forceinline__ void interp_direct(const double *__restrict__ u, const FluidGeom &g,
+                                              int Vi,
                                               int jx, int jy, int jz, const double wx[4],
                                               const double wy[4], const double wz[4],
                                               double &U0, double &U1, double &U2) {
+  const int N1 = g.N1, N2 = g.N2;
   int ro[4][4];
 #pragma unroll
   for (int c = 0; c < 4; ++c)
 #pragma unroll
     for (int b = 0; b < 4; ++b)
-      ro[c][b] = (((jz + c) & (N3 - 1)) * N2 + ((jy + b) & (N2 - 1))) * N1;
+      ro[c][b] = (u_plane(g, jz, c) * N2 + ((jy + b) & (N2 - 1))) * N1;
   U0 = U1 = U2 = 0.0;
   if (jx >= 0 && jx + 3 < N1) {
 #pragma unroll
@@ -429,16 +443,16 @@ constexpr int IMMA_MAXG = 8;
 __global__ void __launch_bounds__(INTERP_THREADS, IBK_IMINB)
 k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
              long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm,
-             const uint8_t *__restrict__ fixed) {
+             const uint8_t *__restrict__ fixed, double4 *pack, unsigned long long *pack_count) {
   // per lane-point: wx[0..3] | wy[0..3] | wz[0], wz[2], wz[1], wz[3]  (+2 pad: odd 16-B stride)
   __shared__ __align__(16) double rec[INTERP_THREADS / 32][32][14];
   __shared__ double uo[INTERP_THREADS / 32][32][3];
   __shared__ unsigned char mlist[INTERP_THREADS / 32][32];   // lanes of the current group
   const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int N1 = g.N1, N2 = g.N2, N3 = g.N3;
-  const int Vi = (int)g.V;
-  const bool live = k < np;
+  const int N1 = g.N1, N2 = g.N2, N3g = g.N3g;
+  const int Vi = (int)((int64_t)N1 * N2 * g.uN3);     // component stride of the u array
+  bool live = k < np;
   bool bad = false;
   const int64_t i = live ? (perm ? (int64_t)__ldg(&perm[k]) : k) : 0;
   double x0 = 0.5 * g.h, x1 = 0.5 * g.h, x2 = 0.5 * g.h;
@@ -447,7 +461,9 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
   const int jx = axis_weights(x0, g.invh, wx);
   const int jy = axis_weights(x1, g.invh, wy);
   const int jz = axis_weights(x2, g.invh, wz);
-  const unsigned key = ((unsigned)(jz & (N3 - 1)) * N2 + (unsigned)(jy & (N2 - 1))) * N1 + (unsigned)(jx & (N1 - 1));
+  // slab: this rank updates only the points whose base plane floor(Z/h) it owns
+  if (g.slab) live = live && ((unsigned)(jz + 1 - g.z0) & (unsigned)(N3g - 1)) < (unsigned)g.N3;
+  const unsigned key = ((unsigned)(jz & (N3g - 1)) * N2 + (unsigned)(jy & (N2 - 1))) * N1 + (unsigned)(jx & (N1 - 1));
   const unsigned active = __ballot_sync(0xffffffffu, live);
   const unsigned peers = __match_any_sync(0xffffffffu, live ? key : 0xffffffffu) & active;
   const unsigned leaders = __ballot_sync(0xffffffffu, live && lane == __ffs(peers) - 1);
@@ -470,8 +486,8 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
       const int gx = __shfl_sync(0xffffffffu, jx, ld), gy = __shfl_sync(0xffffffffu, jy, ld),
                 gz = __shfl_sync(0xffffffffu, jz, ld);
       const int xo = (gx + a) & (N1 - 1), yo = (gy + b) & (N2 - 1);
-      const int e0 = (((gz + c1) & (N3 - 1)) * N2 + yo) * N1 + xo;
-      const int e1 = (((gz + c1 + 2) & (N3 - 1)) * N2 + yo) * N1 + xo;
+      const int e0 = (u_plane(g, gz, c1) * N2 + yo) * N1 + xo;
+      const int e1 = (u_plane(g, gz, c1 + 2) * N2 + yo) * N1 + xo;
       // tile t: component t / 2, c = c1 (t even) or c1 + 2 (t odd)
       double bf[6];
       bf[0] = __ldg(u + e0);          bf[1] = __ldg(u + e1);
@@ -511,7 +527,7 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
     __syncwarp();
     U0 = uo[warp][lane][0]; U1 = uo[warp][lane][1]; U2 = uo[warp][lane][2];
   } else {
-    interp_direct(u, N1, N2, N3, Vi, jx, jy, jz, wx, wy, wz, U0, U1, U2);
+    if (live) interp_direct(u, g, Vi, jx, jy, jz, wx, wy, wz, U0, U1, U2);
   }
   if (live) {
     if (U_out) {
@@ -520,6 +536,19 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
       const double y0 = x0 + g.dt * U0, y1 = x1 + g.dt * U1, y2 = x2 + g.dt * U2;
       X[3 * i + 0] = y0; X[3 * i + 1] = y1; X[3 * i + 2] = y2;
       bad = !(isfinite(y0) && isfinite(y1) && isfinite(y2));
+    }
+  }
+  // slab: the owned points' X^{n+1} (fixed ones included, unchanged) are packed for the
+  // all-gather that keeps every rank's replica of X current
+  if (pack && !U_out) {
+    const unsigned own = __ballot_sync(0xffffffffu, live);
+    unsigned long long base = 0;
+    if (own) {
+      if (lane == __ffs(own) - 1) base = atomicAdd(pack_count, (unsigned long long)__popc(own));
+      base = __shfl_sync(0xffffffffu, base, __ffs(own) - 1);
+      if (live)
+        pack[base + __popc(own & ((1u << lane) - 1u))] =
+            make_double4(X[3 * i + 0], X[3 * i + 1], X[3 * i + 2], (double)i);
     }
   }
   // warp-level vote: a block-wide barrier here made every warp wait for the block's slowest
@@ -531,10 +560,11 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
 
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
-                          const int *perm, const uint8_t *fixed, cudaStream_t s) {
+                          const int *perm, const uint8_t *fixed, cudaStream_t s,
+                          double4 *pack, unsigned long long *pack_count) {
   if (np > 0)
     k_interp_mma<<<(unsigned)((np + INTERP_THREADS - 1) / INTERP_THREADS), INTERP_THREADS, 0, s>>>(
-        g, u, X, np, U_out, flag, dev_n, n, perm, fixed);
+        g, u, X, np, U_out, flag, dev_n, n, perm, fixed, pack, pack_count);
   return cudaGetLastError();
 }
 
@@ -649,16 +679,16 @@ __global__ void k_bin_scatter(const double *__restrict__ X, int64_t np, double i
 cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
                        unsigned *bsum, int *perm, cudaStream_t s) {
   if (np <= 0) return cudaSuccess;
-  const size_t n = (size_t)g.V;
+  const size_t n = (size_t)g.Vg;                  // cells of the whole lattice
   const int nb = (int)((n + (size_t)SCAN_T * SCAN_E - 1) / ((size_t)SCAN_T * SCAN_E));
   const unsigned pb = (unsigned)((np + 255) / 256);
   cudaError_t e = cudaMemsetAsync(cnt, 0, n * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
-  k_bin_count<<<pb, 256, 0, s>>>(X, np, g.invh, g.N1, g.N2, g.N3, cnt);
+  k_bin_count<<<pb, 256, 0, s>>>(X, np, g.invh, g.N1, g.N2g, g.N3g, cnt);
   k_scan_partial<<<nb, SCAN_T, 0, s>>>(cnt, n, bsum);
   k_scan_bsum<<<1, SCAN_T, 0, s>>>(bsum, nb);
   k_scan_final<<<nb, SCAN_T, 0, s>>>(cnt, n, bsum);
-  k_bin_scatter<<<pb, 256, 0, s>>>(X, np, g.invh, g.N1, g.N2, g.N3, cnt, perm);
+  k_bin_scatter<<<pb, 256, 0, s>>>(X, np, g.invh, g.N1, g.N2g, g.N3g, cnt, perm);
   return cudaGetLastError();
 }
 

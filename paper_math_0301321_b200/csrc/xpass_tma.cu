@@ -77,7 +77,9 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
   double2 *stage0 = smraw + ((1024u - (smem_u32(smraw) & 1023u)) & 1023u) / 16u;
   constexpr size_t SW = K::SI / 16;
   const int ntiles = N3 * NYB;
-  const size_t V = (size_t)g.V;
+  // output u array: uN3 planes, local plane z at uz0 + z (slab: ghost planes around)
+  const size_t Vu = (size_t)N * N2 * g.uN3;
+  const int uz0 = g.uz0;
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) { mbar_init(&full[s], 1); mbar_init(&done[s], 1); }
     fence_mbar_init();
@@ -129,7 +131,7 @@ k_xinv_tma(FluidGeom g, const __grid_constant__ CUtensorMap map_main,
     };
     mbar_wait(&full[s], (i / S) & 1);
     const double2 nyq = sm[(size_t)3 * RB * M + comp * K::NQ + row];
-    double2 *o2 = reinterpret_cast<double2 *>(out + comp * V + ((size_t)z * N2 + (y0 + row)) * N);
+    double2 *o2 = reinterpret_cast<double2 *>(out + comp * Vu + ((size_t)(uz0 + z) * N2 + (y0 + row)) * N);
     auto ld = [&](int e) -> double2 {
       double2 Xk = X_at(e), Xm = e == 0 ? nyq : X_at(M - e);
       if (e == 0) { Xk.y = 0.0; Xm.y = 0.0; }      // X_0, X_{N/2} are real

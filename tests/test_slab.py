@@ -1,0 +1,163 @@
+"""Slab decomposition of the IB step along z.
+
+GPU: P slab contexts in one process (device copies in place of the collectives,
+paper_math_0301321_b200.slab.LocalSlabs) against the oracle at checkpoints 1, 2 and 10 on
+BASELINE.json configs[2] (128^3) and configs[3] (256^3) and a small sheet, P = 2, 4 (8).
+CPU: the exchange plumbing (exchange_dist over torch.distributed) on a gloo world of size 2
+against the single-process exchange (exchange_local) on the same buffers.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+
+from gen import make_config, small_sheet_config
+from parity import rel_l2, step_parity
+
+
+# ------------------------------------------------------------------ exchange plumbing (CPU)
+class _FakeRank:
+    """The SlabRank buffer attributes on CPU tensors, filled from a seed per rank."""
+
+    def __init__(self, N, P, rank, cap=64):
+        from paper_math_0301321_b200.slab import slab_shapes
+        g = torch.Generator().manual_seed(1000 + rank)
+        sh = slab_shapes(N, P)
+        self.P, self.rank, self.cap = P, rank, cap
+        self.s2 = torch.randn(sh["s2"], generator=g, dtype=torch.float64)
+        self.z = torch.zeros(sh["z"], dtype=torch.float64)
+        self.edge_send = torch.randn(sh["edge_send"], generator=g, dtype=torch.float64)
+        self.edge_recv = torch.zeros(sh["edge_recv"], dtype=torch.float64)
+        k = 5 + 7 * rank
+        self.pack_send = torch.zeros((cap, 4), dtype=torch.float64)
+        self.pack_send[:k] = torch.randn((k, 4), generator=g, dtype=torch.float64)
+        self.pack_recv = torch.zeros((P, cap, 4), dtype=torch.float64)
+        self.count_send = torch.tensor([k], dtype=torch.int64)
+        self.count_recv = torch.zeros(P, dtype=torch.int64)
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, ws, port, N, q):
+    import torch.distributed as dist
+    from paper_math_0301321_b200.slab import exchange_dist, exchange_local
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    try:
+        me = _FakeRank(N, ws, rank)
+        ref = [_FakeRank(N, ws, r) for r in range(ws)]       # every rank's buffers, locally
+        ok = True
+        for ph in range(4):
+            exchange_dist(me, ph)
+            exchange_local(ref, ph)
+            for name in ("s2", "z", "edge_recv", "count_recv"):
+                ok &= torch.equal(getattr(me, name), getattr(ref[rank], name))
+            for r in range(ws):
+                k = int(ref[r].count_send[0])
+                ok &= torch.equal(me.pack_recv[r, :k], ref[rank].pack_recv[r, :k])
+        # after the forward and the backward transpose s2 is back to its start
+        ok &= torch.equal(me.s2, _FakeRank(N, ws, rank).s2)
+        q.put((rank, bool(ok)))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("N", [(64, 64, 64), (64, 128, 32)])
+def test_slab_exchange_plumbing_gloo_world2(N):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_worker, args=(r, 2, port, N, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    assert res == {0: True, 1: True}
+
+
+def test_slab_transpose_is_the_z_pencil_layout():
+    """After the y -> z exchange, rank q's z[c][src][ky][zl] holds S2 row ky = q Ky + ky of
+    plane z = src L + zl: the z pass's 5-D view (x, zl, ky, src, comp) reads whole pencils."""
+    from paper_math_0301321_b200.slab import exchange_local
+    N, P = (64, 64, 64), 4
+    ranks = [_FakeRank(N, P, r) for r in range(P)]
+    exchange_local(ranks, 0)
+    L, Ky = 64 // P, 64 // P
+    # global S2 [comp][ky][z] from the ranks' local S2 [comp][ky][zl]
+    glob = torch.cat([r.s2.reshape(3, 64, L, -1, 2) for r in ranks], dim=2)   # [3][ky][z]
+    for q in range(P):
+        zq = ranks[q].z                                      # [3][src][Ky][L]
+        pencil = zq.permute(0, 2, 1, 3, 4, 5).reshape(3, Ky, 64, -1, 2)
+        assert torch.equal(pencil, glob[:, q * Ky:(q + 1) * Ky])
+
+
+# ------------------------------------------------------------------ GPU parity
+@pytest.fixture(scope="module")
+def slabm():
+    from paper_math_0301321_b200 import _build, ib
+    _build.build()
+    ib.load()
+    from paper_math_0301321_b200 import slab
+    return slab
+
+
+def _slab_parity(slabm, olib, cfg, P):
+    rep = step_parity(olib, cfg, lambda: slabm.LocalSlabs(cfg, P), check_U=False)
+    return rep
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_slab_small_sheet_matches_oracle(slabm, olib, P):
+    cfg = small_sheet_config(N=64, n1=40, n2=30, seed=61, u_amp=0.2)
+    print(_slab_parity(slabm, olib, cfg, P))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_config3_matches_oracle(slabm, olib, P):
+    print(_slab_parity(slabm, olib, make_config(3), P))
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+@pytest.mark.parametrize("P", [2, 4])
+def test_slab_config4_matches_oracle(slabm, olib, P):
+    print(_slab_parity(slabm, olib, make_config(4), P))
+
+
+@pytest.mark.gpu
+def test_slab_replicas_agree_and_match_the_whole_lattice(slabm):
+    """Every rank's replica of X is the same after the all-gather, and the decomposed step
+    agrees with the one-context step to fp64 summation order."""
+    from paper_math_0301321_b200 import IBContext
+    cfg = small_sheet_config(N=(64, 128, 64), n1=30, n2=24, seed=62, u_amp=0.3)
+    with slabm.LocalSlabs(cfg, 4) as s, IBContext.from_config(cfg) as c:
+        s.step(6)
+        c.step(6)
+        Xs = [s.get_positions(r) for r in range(4)]
+        for X in Xs[1:]:
+            assert np.array_equal(X, Xs[0])
+        us, _ = s.get_fields()
+        uc, _ = c.get_fields()
+        assert rel_l2(us, uc) < 1e-13
+        assert rel_l2(Xs[0] - cfg.X, c.get_positions() - cfg.X) < 1e-11
+        assert s.n == c.n == 6
+
+
+@pytest.mark.gpu
+def test_slab_rejects_bad_decompositions(slabm):
+    from paper_math_0301321_b200.ib import IBError
+    for N, P in (((64, 64, 64), 16), ((64, 64, 64), 3), ((32, 64, 64), 2)):
+        with pytest.raises(IBError):
+            slabm.SlabRank(N, 1 / N[0], 1.0, 0.01, 1e-3, P, 0, 10)
