@@ -24,10 +24,14 @@ namespace ibk {
 #ifndef IBK_XRB
 #define IBK_XRB 32   // rows x threads-per-pencil: RB = 4 rows at N1 = 256 (5 CTAs per SM)
 #endif
+#ifndef IBK_XRB512
+#define IBK_XRB512 32   // the same product at N1 = 512: RB = 2 rows
+#endif
 template <int N> struct XCfg {      // x passes: RB rows of one z-plane per CTA
   static constexpr int M = N / 2;
   static constexpr int T = Plan<M>::T;
-  static constexpr int RB = (IBK_XRB / T) < N ? (IBK_XRB / T) : N;
+  static constexpr int RBT = N >= 512 ? IBK_XRB512 : IBK_XRB;
+  static constexpr int RB = (RBT / T) < N ? (RBT / T) : N;
 };
 #ifndef IBK_YC
 #define IBK_YC 8
@@ -102,7 +106,7 @@ cudaError_t init_tables(ib_ctx *c) {
 // vs 287 us at 256^3 with 4; 6 spill); 4 at N1 = 512, whose 48 KB tiles fit only 4 per SM
 // anyway (2407 vs 2620 us at 512^3 with the 128-register cap)
 #ifndef IBK_XMINB
-#define IBK_XMINB (N >= 512 ? 4 : 5)
+#define IBK_XMINB (N >= 512 ? (XCfg<N>::RB >= 4 ? 3 : 4) : 5)
 #endif
 template <int N, int MODE>
 __global__ void __launch_bounds__(3 * XCfg<N>::RB * XCfg<N>::T, IBK_XMINB)
@@ -173,17 +177,8 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
     const double2 v1 = *reinterpret_cast<const double2 *>(ut + (1 * UR + row + 1) * N + x);
     const double2 v2 = *reinterpret_cast<const double2 *>(ut + (2 * UR + row + 1) * N + x);
     const double2 c = comp == 0 ? v0 : (comp == 1 ? v1 : v2);
-#ifndef IBK_XSWAP
-#define IBK_XSWAP 1
-#endif
-    // x neighbours (8-byte loads, served per half-warp = two rows of one component): odd
-    // rows fetch them in the opposite order, so the two rows of a half-warp hit the
-    // disjoint bank halves of x - 1 and x + 2 instead of the same one (2-way conflict)
-    const int ixm = (x + N - 1) & (N - 1), ixp = (x + 2) & (N - 1);
-    const bool sw = IBK_XSWAP && (row & 1);
-    const double l0 = own[sw ? ixp : ixm];
-    const double l1 = own[sw ? ixm : ixp];
-    const double xm = sw ? l1 : l0, xp = sw ? l0 : l1;
+    const double xm = own[(x + N - 1) & (N - 1)];
+    const double xp = own[(x + 2) & (N - 1)];
     const double2 a_ym = *reinterpret_cast<const double2 *>(own - N + x);
     const double2 a_yp = *reinterpret_cast<const double2 *>(own + N + x);
     const double2 a_zm = __ldg(reinterpret_cast<const double2 *>(uc_ + zm + x));
@@ -513,6 +508,15 @@ static cudaError_t launch_xinv_n(const FluidGeom &g, const double2 *spec, double
   k_xinv<N><<<grid, ncomp * X::RB * X::T, smem, s>>>(g, spec, out, ncomp, twN, twM, flag,
                                                      dev_n, n);
   return cudaGetLastError();
+}
+
+// rows per x-pass tile (XCfg<N1>::RB): ib_create3 requires N2 to be a multiple of it
+int xfwd_rows(int N1) {
+  switch (N1) {
+    case 8: return XCfg<8>::RB;      case 16: return XCfg<16>::RB;    case 32: return XCfg<32>::RB;
+    case 64: return XCfg<64>::RB;    case 128: return XCfg<128>::RB;  case 256: return XCfg<256>::RB;
+    case 512: return XCfg<512>::RB;  default: return 0;
+  }
 }
 
 // ------------------------------------------------------------------ dispatch

@@ -200,11 +200,12 @@ const char *ib_last_error(void) { return g_err.c_str(); }
 
 static bool pow2_in(int32_t n, int32_t lo, int32_t hi) { return n >= lo && n <= hi && !(n & (n - 1)); }
 
-// rows per x-pass tile for a row length N1 (= XCfg<N1>::RB): the y extent N2 must be a
-// multiple of it
+// rows per x-pass tile for a row length N1: the y extent N2 must be a multiple of the
+// forward pass's (fluid.cu XCfg) and of the TMA inverse pass's (xpass_tma.cu XT) row block
 static int32_t x_rows(int32_t N1) {
-  const int32_t M = N1 / 2, T = M >= 16 ? M / 16 : 1, rb = 32 / T;
-  return rb < N1 ? rb : N1;
+  const int32_t a = xfwd_rows(N1);
+  const int32_t M = N1 / 2, T = M >= 16 ? M / 16 : 1, b = 32 / T < N1 ? 32 / T : N1;
+  return a > b ? a : b;
 }
 
 ib_ctx *ib_create3(int32_t N1, int32_t N2, int32_t N3, double h, double rho, double mu,

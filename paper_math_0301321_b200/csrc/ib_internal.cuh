@@ -168,6 +168,7 @@ inline int sm_count() {
 }
 // kernels/launchers (fluid.cu)
 cudaError_t init_tables(ib_ctx *c);
+int xfwd_rows(int N1);   // rows per x-pass tile: N2 must be a multiple
 // twiddles and symbols of one lattice axis of length N (slab contexts: the whole z axis)
 cudaError_t init_axis_table(double2 *twN, int N, double *s, double *l, double h, cudaStream_t st);
 cudaError_t fluid_setup_attributes(int N);

@@ -119,7 +119,8 @@ def _slab_parity(slabm, olib, cfg, P):
 @pytest.mark.gpu
 @pytest.mark.parametrize("P", [2, 4, 8])
 def test_slab_small_sheet_matches_oracle(slabm, olib, P):
-    cfg = small_sheet_config(N=64, n1=40, n2=30, seed=61, u_amp=0.2)
+    # dt 2.5e-4: the sheet's stiffest springs and tethers are unstable at dt 1e-3 on h = 1/64
+    cfg = small_sheet_config(N=64, n1=40, n2=30, seed=61, u_amp=0.2, dt=2.5e-4)
     print(_slab_parity(slabm, olib, cfg, P))
 
 
@@ -141,7 +142,7 @@ def test_slab_replicas_agree_and_match_the_whole_lattice(slabm):
     """Every rank's replica of X is the same after the all-gather, and the decomposed step
     agrees with the one-context step to fp64 summation order."""
     from paper_math_0301321_b200 import IBContext
-    cfg = small_sheet_config(N=(64, 128, 64), n1=30, n2=24, seed=62, u_amp=0.3)
+    cfg = small_sheet_config(N=(64, 128, 64), n1=30, n2=24, seed=62, u_amp=0.3, dt=2.5e-4)
     with slabm.LocalSlabs(cfg, 4) as s, IBContext.from_config(cfg) as c:
         s.step(6)
         c.step(6)
