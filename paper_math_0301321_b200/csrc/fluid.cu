@@ -132,6 +132,9 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   const size_t V = (size_t)g.V;
   const size_t rowbase = ((size_t)z * N2 + y) * N;
   const double cu = g.rho / g.dt, ra = g.rho * g.invh;
+  // F is only read on rows the spread touched (row flags), else taken as 0; the flag is
+  // loaded before the tile wait so that its latency overlaps the TMA transfer
+  const unsigned rflag = (MODE == 0 && rowflag) ? rowflag[(size_t)z * N2 + y] : 1u;
   if (MODE != 2 && use_tma) {   // one thread streams the 3 x (RB + 2) rows with TMA
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
@@ -158,8 +161,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
     cp_async_wait_all();
     __syncthreads();
   }
-  // F is only read on rows the spread touched (row flags), else taken as 0
-  const bool hasF = MODE == 1 || (MODE == 0 && (rowflag == nullptr || rowflag[(size_t)z * N2 + y] != 0));
+  const bool hasF = MODE == 1 || (MODE == 0 && rflag != 0);
   // z -+ 1: periodic on the whole lattice; in a slab the neighbours are ghost planes
   const int zmi = g.slab ? zu - 1 : ((z + N3 - 1) & (N3 - 1));
   const int zpi = g.slab ? zu + 1 : ((z + 1) & (N3 - 1));
