@@ -545,3 +545,31 @@ def test_strip_experiment_observables_match_oracle(ibm, olib):
     assert eo.max() > 0
     assert np.max(np.abs(eg - eo)) <= 1e-9 * eo.max()
     assert ex.peak_location(eg, s) == ex.peak_location(eo, s)
+
+
+def test_spread_interp_degenerate_positions(ibm, olib):
+    """Points exactly on lattice nodes, on cell faces and edges (floor(X/h) exact, the window
+    j0 = floor - 1 .. + 2 with phi(+-2) = 0 at its ends, reading Z8), exactly on
+    the periodic boundary, negative and far outside the box (indices mod N), and many
+    points coinciding: spread and interpolation against the oracle, plus adjointness."""
+    N = 32
+    h = 1.0 / N
+    rng = np.random.default_rng(71)
+    nodes = rng.integers(-3 * N, 4 * N, (200, 3)) * h                 # on nodes, any period
+    faces = rng.integers(0, N, (200, 3)) * h
+    faces[:, 0] += 0.5 * h                                              # x between nodes
+    edges = np.array([[0.0, 0.0, 0.0], [1.0, 1.0, 1.0], [1.0 - 1e-16, 0.5, 0.5],
+                      [-1e-300, 0.25, 0.75], [31 * h, 31 * h, 31 * h], [-h, -h, -h]])
+    same = np.tile([[0.4375, 0.5, 0.53125]], (70, 1))                  # 70 coincident points
+    X = np.ascontiguousarray(np.concatenate([nodes, faces, edges, same]))
+    f = rng.standard_normal(X.shape)
+    u = rng.standard_normal((3, N, N, N))
+    patches, st = _points_only(X)
+    with _ctx(ibm, N, X=X, patches=patches, stiff=st) as c:
+        F = c.debug_spread(f)
+        U = c.debug_interp(u)
+    Fo = olib.spread(N, h, X, f)
+    Uo = olib.interp(N, h, u, X)
+    assert rel_l2(F, Fo) < 1e-13
+    assert np.max(np.abs(U - Uo)) <= 1e-13 * np.max(np.abs(Uo))
+    assert abs(np.sum(F * u) * h ** 3 - np.sum(f * U)) <= 1e-12 * np.sum(np.abs(f * U))
