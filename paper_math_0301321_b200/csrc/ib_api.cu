@@ -52,7 +52,8 @@ int count_nonfinite(ib_ctx *c, const double *d, size_t n, unsigned long long *ou
 
 StructDev struct_dev(const ib_ctx *c) {
   StructDev s;
-  s.X = c->X; s.np = c->np; s.perm = c->since_bin >= 0 ? c->perm : nullptr; s.patches = c->patches; s.npatch = c->npatch; s.stiff = c->stiff;
+  s.X = c->X; s.np = c->np; s.perm = c->since_bin >= 0 ? c->perm : nullptr;
+  s.Xs = c->since_bin >= 0 ? c->Xs : nullptr; s.patches = c->patches; s.npatch = c->npatch; s.stiff = c->stiff;
   s.nd = c->nd; s.drive_idx = c->drive_idx; s.drive_dir = c->drive_dir;
   s.drive_amp = c->drive_amp; s.drive_period = c->drive_period;
   return s;
@@ -125,10 +126,10 @@ cudaError_t xinv(ib_ctx *c, double *out, const long long *dev_n, long long n, lo
 // (Re)bin the points by base cell when the permutation is missing or SORT_PERIOD steps old.
 cudaError_t ensure_binned(ib_ctx *c, cudaStream_t s) {
   if (c->np == 0 || (c->since_bin >= 0 && c->since_bin < SORT_PERIOD)) return cudaSuccess;
-  cudaError_t e = launch_bin(c->g, c->X, c->np, c->bincnt, c->binsum, c->perm, s);
+  cudaError_t e = launch_bin(c->g, c->X, c->np, c->bincnt, c->binsum, c->perm, c->Xs, s);
   if (e == cudaSuccess) {
     c->since_bin = 0;
-    c->launches += 5;
+    c->launches += 6;
   }
   return e;
 }
@@ -156,7 +157,8 @@ cudaError_t enqueue_step(ib_ctx *c, bool pressure, cudaEvent_t *ev) {
   mark(5);
   if ((e = xinv(c, c->u, dev_n, n, c->flag, s)) != cudaSuccess) return e;
   mark(6);
-  if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, sd.perm, c->fixed, s)) != cudaSuccess) return e;
+  if ((e = launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, dev_n, n, sd.perm, c->fixed, s,
+                         nullptr, nullptr, c->Xs)) != cudaSuccess) return e;
   mark(7);
   return launch_step_inc(c->dev_n, s);
 }
@@ -290,7 +292,7 @@ void ib_destroy(ib_ctx *c) {
   for (int a = 0; a < 3; ++a) { dfree(c->tw[a]); dfree(c->sym_s[a]); dfree(c->sym_l[a]); }
   dfree(c->twM);
   dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->drive_idx); dfree(c->drive_dir);
-  dfree(c->perm); dfree(c->bincnt); dfree(c->binsum); dfree(c->fixed);
+  dfree(c->perm); dfree(c->Xs); dfree(c->bincnt); dfree(c->binsum); dfree(c->fixed);
   dfree(c->flag); dfree(c->dev_n);
   if (c->flag_h) cudaFreeHost(c->flag_h);
   for (int k = 0; k <= STAGE_COUNT; ++k) if (c->ev[k]) cudaEventDestroy(c->ev[k]);
@@ -384,11 +386,12 @@ int ib_set_structure(ib_ctx *c, const double *points, int64_t np, const ib_patch
   // upload
   free_graph(c);
   CK(cudaStreamSynchronize(c->stream));
-  dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->perm);
-  c->X = nullptr; c->patches = nullptr; c->stiff = nullptr; c->perm = nullptr;
+  dfree(c->X); dfree(c->patches); dfree(c->stiff); dfree(c->perm); dfree(c->Xs);
+  c->X = nullptr; c->patches = nullptr; c->stiff = nullptr; c->perm = nullptr; c->Xs = nullptr;
   c->since_bin = -1;
   CK(dalloc(&c->X, (size_t)np * 3));
   CK(dalloc(&c->perm, (size_t)np));
+  CK(dalloc(&c->Xs, (size_t)np * 3));
   if (np > 0 && !c->bincnt) {
     CK(dalloc(&c->bincnt, (size_t)c->g.Vg));            // cells of the whole lattice
     CK(dalloc(&c->binsum, (size_t)bin_scan_blocks(c->g.Vg)));
@@ -678,7 +681,9 @@ int ib_debug_interp(ib_ctx *c, const double *u, double *U_out) {
   CK(t.get(&U, (size_t)c->np * 3));
   CK(copy_sync(ud, u, 3 * V * sizeof(double), c->stream));
   CK(ensure_binned(c, c->stream));
-  CK(launch_interp(c->g, ud, c->X, c->np, U, nullptr, nullptr, 0, struct_dev(c).perm, nullptr, c->stream));
+  const StructDev sd = struct_dev(c);
+  CK(launch_interp(c->g, ud, c->X, c->np, U, nullptr, nullptr, 0, sd.perm, nullptr, c->stream,
+                   nullptr, nullptr, c->Xs));
   CK(copy_sync(U_out, U, (size_t)c->np * 3 * sizeof(double), c->stream));
   return IB_OK;
 }

@@ -17,6 +17,7 @@ struct StructDev {
   const double *X;            // [np][3]
   int64_t np;
   const int *perm;            // cell-binned visiting order of the points (or null)
+  const double *Xs;           // [3][np] positions in that order (SoA; with perm, else null)
   const ib_patch *patches;    // [npatch]
   int32_t npatch;
   const double *stiff;
@@ -103,6 +104,7 @@ struct ib_ctx {
   int64_t np = 0;
   double *X = nullptr;
   int *perm = nullptr;          // [np] cell-binned order (binning scratch: bincnt [V], binsum)
+  double *Xs = nullptr;         // [3][np] X in perm order (coalesced reads in spread / interp)
   unsigned *bincnt = nullptr, *binsum = nullptr;
   int64_t since_bin = -1;       // steps since the last binning (-1: perm invalid)
   ib_patch *patches = nullptr;
@@ -216,13 +218,18 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g,
 // fixed (may be null): points with fixed[i] != 0 are not moved
 // pack (slab, may be null): the owned points' X^{n+1} as (x, y, z, index) records, counted
 // in *pack_count
+// Xs (may be null; needs perm): the perm-ordered SoA copy of X, read and kept in step
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
                           const int *perm, const uint8_t *fixed, cudaStream_t s,
-                          double4 *pack = nullptr, unsigned long long *pack_count = nullptr);
-// cell binning: perm = point indices grouped by base cell (5 launches + 1 memset)
+                          double4 *pack = nullptr, unsigned long long *pack_count = nullptr,
+                          double *Xs = nullptr);
+// cell binning: perm = point indices grouped by base cell, Xs = X in that order as SoA
+// (6 launches + 1 memset)
 cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
-                       unsigned *bsum, int *perm, cudaStream_t s);
+                       unsigned *bsum, int *perm, double *Xs, cudaStream_t s);
+cudaError_t launch_gather_xs(const double *X, const int *perm, int64_t np, double *Xs,
+                             cudaStream_t s);
 int bin_scan_blocks(int64_t V);
 cudaError_t launch_step_inc(long long *dev_n, cudaStream_t s);
 constexpr int SORT_PERIOD = 32;   // steps between re-binnings inside ib_step

@@ -64,9 +64,10 @@ __device__ __forceinline__ void spring(const double *__restrict__ X, double xi, 
   f[2] += t * dz;
 }
 
-// pt: the patch table (shared-memory copy when it fits, else sd.patches)
+// pt: the patch table (shared-memory copy when it fits, else sd.patches); xyz: the point's
+// own position, already loaded by the caller
 __device__ __forceinline__ void point_force(const StructDev &sd, const ib_patch *pt, int64_t i,
-                                            double f[3], double xyz[3]) {
+                                            double f[3], const double xyz[3]) {
   int lo = 0, hi = sd.npatch - 1;
   while (lo < hi) {
     const int mid = (lo + hi + 1) >> 1;
@@ -81,9 +82,7 @@ __device__ __forceinline__ void point_force(const StructDev &sd, const ib_patch 
   // 32-bit index arithmetic: a patch holds < 2^31 points (ib_set_structure checks np)
   const int i2 = (int)((unsigned)li / (unsigned)n1), i1 = (int)li - i2 * n1;
   const double *b = sd.stiff + P->param_off;
-  const double xi = __ldg(&sd.X[3 * i + 0]), yi = __ldg(&sd.X[3 * i + 1]),
-               zi = __ldg(&sd.X[3 * i + 2]);
-  xyz[0] = xi; xyz[1] = yi; xyz[2] = zi;
+  const double xi = xyz[0], yi = xyz[1], zi = xyz[2];
   f[0] = f[1] = f[2] = 0.0;
 #pragma unroll
   for (int fam = 0; fam < 4; ++fam) {
@@ -163,7 +162,8 @@ __device__ __forceinline__ double drive_factor(const StructDev &sd, long long n)
 __global__ void k_force(StructDev sd, const long long *dev_n, long long n, double *f_out) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= sd.np) return;
-  double f[3], xyz[3];
+  double f[3];
+  const double xyz[3] = {__ldg(&sd.X[3 * i + 0]), __ldg(&sd.X[3 * i + 1]), __ldg(&sd.X[3 * i + 2])};
   point_force(sd, sd.patches, i, f, xyz);
   f_out[3 * i + 0] = f[0];
   f_out[3 * i + 1] = f[1];
@@ -269,9 +269,13 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
     bool live = false;
     if (k < sd.np) {
       double f[3], xyz[3];
+      if (sd.Xs) {             // binned SoA copy: coalesced (the AoS X[i] is 1 sector per lane)
+        xyz[0] = __ldg(&sd.Xs[k]); xyz[1] = __ldg(&sd.Xs[sd.np + k]); xyz[2] = __ldg(&sd.Xs[2 * sd.np + k]);
+      } else {
+        xyz[0] = __ldg(&sd.X[3 * i + 0]); xyz[1] = __ldg(&sd.X[3 * i + 1]); xyz[2] = __ldg(&sd.X[3 * i + 2]);
+      }
       if (FROM_ARRAY) {
         f[0] = __ldg(&f_in[3 * i]); f[1] = __ldg(&f_in[3 * i + 1]); f[2] = __ldg(&f_in[3 * i + 2]);
-        xyz[0] = __ldg(&sd.X[3 * i + 0]); xyz[1] = __ldg(&sd.X[3 * i + 1]); xyz[2] = __ldg(&sd.X[3 * i + 2]);
       } else {
         point_force(sd, pt, i, f, xyz);
       }
@@ -443,7 +447,8 @@ constexpr int IMMA_MAXG = 8;
 __global__ void __launch_bounds__(INTERP_THREADS, IBK_IMINB)
 k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, double *U_out,
              long long *flag, const long long *dev_n, long long n, const int *__restrict__ perm,
-             const uint8_t *__restrict__ fixed, double4 *pack, unsigned long long *pack_count) {
+             const uint8_t *__restrict__ fixed, double4 *pack, unsigned long long *pack_count,
+             double *Xs) {
   // per lane-point: wx[0..3] | wy[0..3] | wz[0], wz[2], wz[1], wz[3]  (+2 pad: odd 16-B stride)
   __shared__ __align__(16) double rec[INTERP_THREADS / 32][32][14];
   __shared__ double uo[INTERP_THREADS / 32][32][3];
@@ -456,7 +461,10 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
   bool bad = false;
   const int64_t i = live ? (perm ? (int64_t)__ldg(&perm[k]) : k) : 0;
   double x0 = 0.5 * g.h, x1 = 0.5 * g.h, x2 = 0.5 * g.h;
-  if (live) { x0 = X[3 * i + 0]; x1 = X[3 * i + 1]; x2 = X[3 * i + 2]; }
+  if (live) {
+    if (Xs) { x0 = Xs[k]; x1 = Xs[np + k]; x2 = Xs[2 * np + k]; }   // binned SoA: coalesced
+    else { x0 = X[3 * i + 0]; x1 = X[3 * i + 1]; x2 = X[3 * i + 2]; }
+  }
   double wx[4], wy[4], wz[4];
   const int jx = axis_weights(x0, g.invh, wx);
   const int jy = axis_weights(x1, g.invh, wy);
@@ -535,6 +543,7 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
     } else if (!(fixed && fixed[i])) {    // fixed points never move (PAPER.md 919-920)
       const double y0 = x0 + g.dt * U0, y1 = x1 + g.dt * U1, y2 = x2 + g.dt * U2;
       X[3 * i + 0] = y0; X[3 * i + 1] = y1; X[3 * i + 2] = y2;
+      if (Xs) { Xs[k] = y0; Xs[np + k] = y1; Xs[2 * np + k] = y2; }
       bad = !(isfinite(y0) && isfinite(y1) && isfinite(y2));
     }
   }
@@ -561,10 +570,10 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
 cudaError_t launch_interp(const FluidGeom &g, const double *u, double *X, int64_t np,
                           double *U_out, long long *flag, const long long *dev_n, long long n,
                           const int *perm, const uint8_t *fixed, cudaStream_t s,
-                          double4 *pack, unsigned long long *pack_count) {
+                          double4 *pack, unsigned long long *pack_count, double *Xs) {
   if (np > 0)
     k_interp_mma<<<(unsigned)((np + INTERP_THREADS - 1) / INTERP_THREADS), INTERP_THREADS, 0, s>>>(
-        g, u, X, np, U_out, flag, dev_n, n, perm, fixed, pack, pack_count);
+        g, u, X, np, U_out, flag, dev_n, n, perm, fixed, pack, pack_count, perm ? Xs : nullptr);
   return cudaGetLastError();
 }
 
@@ -676,8 +685,23 @@ __global__ void k_bin_scatter(const double *__restrict__ X, int64_t np, double i
   if (ok) perm[base + __popc(peers & ((1u << lane) - 1u))] = (int)i;
 }
 
+__global__ void k_gather_xs(const double *__restrict__ X, const int *__restrict__ perm,
+                            int64_t np, double *Xs) {
+  const int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < np) {
+    const int64_t i = perm[k];
+    Xs[k] = X[3 * i]; Xs[np + k] = X[3 * i + 1]; Xs[2 * np + k] = X[3 * i + 2];
+  }
+}
+
+cudaError_t launch_gather_xs(const double *X, const int *perm, int64_t np, double *Xs,
+                             cudaStream_t s) {
+  if (np > 0 && Xs) k_gather_xs<<<(unsigned)((np + 255) / 256), 256, 0, s>>>(X, perm, np, Xs);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned *cnt,
-                       unsigned *bsum, int *perm, cudaStream_t s) {
+                       unsigned *bsum, int *perm, double *Xs, cudaStream_t s) {
   if (np <= 0) return cudaSuccess;
   const size_t n = (size_t)g.Vg;                  // cells of the whole lattice
   const int nb = (int)((n + (size_t)SCAN_T * SCAN_E - 1) / ((size_t)SCAN_T * SCAN_E));
@@ -689,7 +713,7 @@ cudaError_t launch_bin(const FluidGeom &g, const double *X, int64_t np, unsigned
   k_scan_bsum<<<1, SCAN_T, 0, s>>>(bsum, nb);
   k_scan_final<<<nb, SCAN_T, 0, s>>>(cnt, n, bsum);
   k_bin_scatter<<<pb, 256, 0, s>>>(X, np, g.invh, g.N1, g.N2g, g.N3g, cnt, perm);
-  return cudaGetLastError();
+  return launch_gather_xs(X, perm, np, Xs, s);
 }
 
 int bin_scan_blocks(int64_t V) {

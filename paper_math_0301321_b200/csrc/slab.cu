@@ -219,7 +219,7 @@ int ib_slab_phase(ib_ctx *c, int32_t phase) {
       CK(cudaMemsetAsync(c->count_send, 0, sizeof(unsigned long long), s));
       CK(launch_interp(g, c->u, c->X, c->np, nullptr, c->flag, c->dev_n, 0,
                        c->since_bin >= 0 ? c->perm : nullptr, c->fixed, s, c->pack_send,
-                       c->count_send));
+                       c->count_send, c->Xs));
       if (c->np > 0) c->launches += 1;
       return IB_OK;
     }
@@ -231,6 +231,10 @@ int ib_slab_phase(ib_ctx *c, int32_t phase) {
                                             c->np);
         CK(cudaGetLastError());
         c->launches += 1;
+        if (c->since_bin >= 0) {                 // the binned copy follows the other ranks' points
+          CK(launch_gather_xs(c->X, c->perm, c->np, c->Xs, s));
+          c->launches += 1;
+        }
       }
       CK(launch_step_inc(c->dev_n, s));
       c->launches += 1;
