@@ -162,3 +162,41 @@ def test_slab_rejects_bad_decompositions(slabm):
     for N, P in (((64, 64, 64), 16), ((64, 64, 64), 3), ((32, 64, 64), 2)):
         with pytest.raises(IBError):
             slabm.SlabRank(N, 1 / N[0], 1.0, 0.01, 1e-3, P, 0, 10)
+
+
+@pytest.mark.gpu
+def test_distslab_nccl_world1_matches_oracle(slabm, olib):
+    """The torch.distributed path (DistSlab: NCCL all_to_all_single / all_gather_into_tensor
+    between the phases) in a world of one rank on the box's one GPU, against the oracle at
+    steps 1, 2, 10.  (Several ranks need several GPUs; the exchange layout for P = 2 is
+    covered by the gloo test above and by LocalSlabs.)"""
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(_free_port()))
+    torch.cuda.set_device(0)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        cfg = small_sheet_config(N=64, n1=40, n2=30, seed=63, u_amp=0.2, dt=2.5e-4)
+
+        class _Run:
+            def __init__(self):
+                self.d = slabm.DistSlab(cfg)
+
+            def step(self, k):
+                self.d.step(k)
+
+            @property
+            def n(self):
+                return self.d.rank.n
+
+            def get_fields(self):
+                return self.d.rank.get_fields()
+
+            def get_positions(self):
+                return self.d.rank.get_positions()
+
+            def close(self):
+                self.d.close()
+
+        print(step_parity(olib, cfg, _Run, check_U=False))
+    finally:
+        dist.destroy_process_group()
