@@ -200,3 +200,18 @@ def test_distslab_nccl_world1_matches_oracle(slabm, olib):
         print(step_parity(olib, cfg, _Run, check_U=False))
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_slab_window_plate_matches_oracle(slabm, olib):
+    """Fixed rim points and the surface-normal drive (PAPER.md 914-922, 988-993) through the
+    slab phases: the normal comes from every rank's replica of X^n; fixed points are owned
+    like any other and never move (bitwise)."""
+    from gen import window_config
+    cfg = window_config(N=64, m=40, seed=9, u_amp=0.05, dt=2.5e-4)
+    print(_slab_parity(slabm, olib, cfg, 2))
+    with slabm.LocalSlabs(cfg, 2) as s:
+        s.step(5)
+        X = s.get_positions(1)
+    fixed = cfg.fixed.astype(bool)
+    assert np.array_equal(X[fixed], cfg.X[fixed])
