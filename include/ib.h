@@ -174,7 +174,8 @@ int ib_slab_info(ib_ctx *ctx, int32_t *info, int32_t cap);
 int ib_slab_set_buffers(ib_ctx *ctx, void *s2, void *z, double *edge_send, double *edge_recv,
                         void *pack_send, void *pack_recv, uint64_t *count_send,
                         uint64_t *count_recv, int64_t pack_cap);
-/* Enqueue phase 0..4 of the next step (see above); phase 4 advances ib_get_step. */
+/* Enqueue phase 0..4 of the next step (see above); phase 4 advances ib_get_step.  Phases
+ * must come in order 0, 1, 2, 3, 4, 0, ... (IB_ESTATE otherwise). */
 int ib_slab_phase(ib_ctx *ctx, int32_t phase);
 /* Synchronise the ctx stream; IB_ENONFINITE (first bad step in ib_last_error) if u or X of
  * this rank became non-finite since the last call. */

@@ -135,6 +135,7 @@ struct ib_ctx {
   // g then describes the local planes (x and y passes, spread, interp), gz the z pass over
   // the received transpose blocks; the exchange buffers belong to the caller.
   int slab_P = 0, slab_rank = 0;
+  int slab_next = 0;            // next ib_slab_phase expected (0..4, cyclic)
   ibk::FluidGeom gz{};
   ibk::TmaMaps zmaps;
   double2 *s2_ext = nullptr, *z_ext = nullptr;   // [3][N2][L][P] / [3][P][Ky][L][P] complex

@@ -174,6 +174,10 @@ int ib_slab_phase(ib_ctx *c, int32_t phase) {
   if (!c->slab_P) return fail(IB_ESTATE, "not a slab context");
   if (!c->z_ext) return fail(IB_ESTATE, "ib_slab_set_buffers first");
   if (c->np > c->pack_cap) return fail(IB_ESTATE, "structure larger than pack_cap");
+  if (phase != c->slab_next)                 // the exchanges between phases assume the order
+    return fail(IB_ESTATE, "slab phase " + std::to_string(phase) + " called, expected " +
+                               std::to_string(c->slab_next));
+  c->slab_next = (c->slab_next + 1) % 5;
   const FluidGeom &g = c->g;
   cudaStream_t s = c->stream;
   const size_t plane = (size_t)g.N1 * g.N2;
@@ -185,7 +189,7 @@ int ib_slab_phase(ib_ctx *c, int32_t phase) {
       CK(launch_force_spread(struct_dev(c), g, nullptr, c->dev_n, 0, c->F, c->rowflag, s));
       CK(xfwd(c, 0, c->u, c->F, c->rowflag, nullptr, s));
       CK(yfwd(c, s));
-      c->launches += 3 + (c->np > 0 ? 1 : 0) + (c->nd > 0 && c->np > 0 ? 1 : 0);
+      c->launches += 2 + (c->np > 0 ? 1 : 0) + (c->nd > 0 && c->np > 0 ? 1 : 0);
       return IB_OK;
     }
     case 1:

@@ -215,3 +215,19 @@ def test_slab_window_plate_matches_oracle(slabm, olib):
         X = s.get_positions(1)
     fixed = cfg.fixed.astype(bool)
     assert np.array_equal(X[fixed], cfg.X[fixed])
+
+
+@pytest.mark.gpu
+def test_slab_phases_must_come_in_order(slabm):
+    from paper_math_0301321_b200.ib import IBError, IB_ESTATE
+    cfg = small_sheet_config(N=64, n1=8, n2=6, seed=64, dt=2.5e-4)
+    r = slabm.SlabRank.from_config(cfg, 2, 0)
+    try:
+        with pytest.raises(IBError) as e:
+            r.phase(1)
+        assert e.value.code == IB_ESTATE
+        r.phase(0)
+        with pytest.raises(IBError):
+            r.phase(0)
+    finally:
+        r.close()
