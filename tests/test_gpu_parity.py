@@ -573,3 +573,29 @@ def test_spread_interp_degenerate_positions(ibm, olib):
     assert rel_l2(F, Fo) < 1e-13
     assert np.max(np.abs(U - Uo)) <= 1e-13 * np.max(np.abs(Uo))
     assert abs(np.sum(F * u) * h ** 3 - np.sum(f * U)) <= 1e-12 * np.sum(np.abs(f * U))
+
+
+@pytest.mark.parametrize("shape", [(64, 64, 512), (128, 64, 512)])
+def test_z512_column_passes(ibm, olib, shape):
+    """The 512-long z pencils (2-column tiles, SWIZZLE_32B, 2 consumer groups; the in-place
+    passes' conflict flips, fluid_tma.cu fft_inplace): forward FFT vs numpy, the fluid step
+    vs the oracle, and the per-mode solve alone (S3c) vs the oracle's solve."""
+    n1, n2, n3 = shape
+    rng = np.random.default_rng(81)
+    x = rng.standard_normal((n3, n2, n1))
+    h, rho, mu, dt = 1.0 / n1, 1.0, 0.02, 1e-3
+    u = random_divfree_velocity(shape, 3, 0.3, rng) + 0.05 * rng.standard_normal((3, n3, n2, n1))
+    F = rng.standard_normal((3, n3, n2, n1)) * 50
+    with ibm.IBContext(shape, h, rho, mu, dt) as c:
+        got = c.debug_fft(x)
+        un, p = c.debug_fluid(u, F)
+        r = rng.standard_normal((3, n3, n2, n1))
+        uh, ph = c.debug_project(np.fft.rfftn(r, axes=(1, 2, 3)))
+        for _ in range(20):                           # deterministic passes: bitwise repeats
+            assert np.array_equal(c.debug_fft(x), got)
+    ref = np.fft.rfftn(x)
+    assert np.max(np.abs(got - ref)) < 1e-13 * np.max(np.abs(ref)) * np.log2(x.size)
+    ref_u, ref_p = olib.fluid_step(shape, h, rho, mu, dt, u, F)
+    assert rel_l2(un, ref_u) < 1e-13 and rel_l2(p, ref_p) < 1e-12
+    us, ps = olib.solve(shape, h, rho, mu, dt, r)
+    assert rel_l2(uh, np.fft.rfftn(us, axes=(1, 2, 3))) < 1e-13
