@@ -174,7 +174,29 @@ struct PassI {
   static constexpr int R = P::radix(PASS), NS = P::ns(PASS), NR = L / R, J = NR / P::T;
 };
 
-template <int L, int SIGN, int PASS, class TW, class LDF>
+// v[r] *= w^(e0 r), r = 1..15, w = exp(SIGN 2 pi i / L), from the four table entries
+// w^e0, w^2e0, w^4e0, w^8e0 and 11 complex products (each power at most three roundings
+// from the table) instead of 15 table reads: the reads' latency (L1 for the global table,
+// shared for a staged one) was the largest stall of the column passes.
+template <int L, int SIGN, class TW>
+__device__ __forceinline__ void twiddle16_pow(double2 *v, int e0, TW tw) {
+  const double2 b0 = twiddle<SIGN>(tw, e0), b1 = twiddle<SIGN>(tw, 2 * e0),
+                b2 = twiddle<SIGN>(tw, 4 * e0), b3 = twiddle<SIGN>(tw, 8 * e0);
+  const double2 p3 = cmul(b0, b1), p12 = cmul(b3, b2);
+  v[1] = cmul(v[1], b0);             v[2] = cmul(v[2], b1);
+  v[3] = cmul(v[3], p3);             v[4] = cmul(v[4], b2);
+  v[5] = cmul(v[5], cmul(b2, b0));   v[6] = cmul(v[6], cmul(b2, b1));
+  v[7] = cmul(v[7], cmul(b2, p3));   v[8] = cmul(v[8], b3);
+  v[9] = cmul(v[9], cmul(b3, b0));   v[10] = cmul(v[10], cmul(b3, b1));
+  v[11] = cmul(v[11], cmul(b3, p3)); v[12] = cmul(v[12], p12);
+  v[13] = cmul(v[13], cmul(p12, b0)); v[14] = cmul(v[14], cmul(p12, b1));
+  v[15] = cmul(v[15], cmul(p12, p3));
+}
+
+// POW: radix-16 passes take their twiddles from twiddle16_pow (4 table reads + products)
+// instead of 15 table reads; chosen per kernel by measurement (it frees the latency-bound
+// x forward and z passes, but costs the register-heavy y passes more than it saves).
+template <int L, int SIGN, int PASS, bool POW = false, class TW, class LDF>
 __device__ __forceinline__ void pass_lc(double2 *v, int t, TW tw, LDF ld) {
   using I = PassI<L, PASS>;
 #pragma unroll
@@ -193,9 +215,13 @@ __device__ __forceinline__ void pass_lc(double2 *v, int t, TW tw, LDF ld) {
     const int j = t + q * Plan<L>::T;
     if (I::NS > 1) {
       const int jm = j % I::NS;
+      if constexpr (I::R == 16 && POW) {
+        twiddle16_pow<L, SIGN>(&v[q * I::R], jm * (L / (I::NS * I::R)), tw);
+      } else {
 #pragma unroll
-      for (int r = 1; r < I::R; ++r)
-        v[q * I::R + r] = cmul(v[q * I::R + r], twiddle<SIGN>(tw, jm * r * (L / (I::NS * I::R))));
+        for (int r = 1; r < I::R; ++r)
+          v[q * I::R + r] = cmul(v[q * I::R + r], twiddle<SIGN>(tw, jm * r * (L / (I::NS * I::R))));
+      }
     }
     dft_reg<I::R, SIGN>(&v[q * I::R]);
   }
@@ -228,7 +254,8 @@ struct NoOp {
   __device__ __forceinline__ void operator()() const {}
 };
 
-template <int L, int SIGN, bool LD_SMEM, bool WARP, class LDF, class STF, class AF = NoOp>
+template <int L, int SIGN, bool LD_SMEM, bool WARP, bool POW = false, class LDF, class STF,
+          class AF = NoOp>
 __device__ __forceinline__ void fft_io(double2 *sp, int t, const double2 *__restrict__ tw,
                                        LDF ld, STF st, AF after_load = AF()) {
   using P = Plan<L>;
@@ -245,14 +272,14 @@ __device__ __forceinline__ void fft_io(double2 *sp, int t, const double2 *__rest
     if (LD_SMEM) pencil_sync<WARP>();
     pass_st<L, 0>(v, t, sst);
     pencil_sync<WARP>();
-    pass_lc<L, SIGN, 1>(v, t, tw, sld);
+    pass_lc<L, SIGN, 1, POW>(v, t, tw, sld);
     if constexpr (P::NPASS == 2) {
       pass_st<L, 1>(v, t, st);
     } else {
       pencil_sync<WARP>();
       pass_st<L, 1>(v, t, sst);
       pencil_sync<WARP>();
-      pass_lc<L, SIGN, 2>(v, t, tw, sld);
+      pass_lc<L, SIGN, 2, POW>(v, t, tw, sld);
       pass_st<L, 2>(v, t, st);
     }
   }

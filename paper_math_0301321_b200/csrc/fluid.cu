@@ -216,7 +216,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   // reads both k and M - k runs without bank conflicts
   auto sst = [sp](int e, double2 v) { sp[e] = v; };
   auto bar = []() { __syncthreads(); };             // u tile dead before pencils alias it
-  fft_io<M, -1, false, true>(sp, t, twM, ld, sst, bar);
+  fft_io<M, -1, false, true, true>(sp, t, twM, ld, sst, bar);   // power twiddles (measured)
   __syncthreads();
   if (MODE == 0 && rowflag && threadIdx.x < RB) rowflag[(size_t)z * N2 + y0 + threadIdx.x] = 0u;
   // split the length-M transform Z of z_n = r_2n + i r_2n+1 into X_k, k = 0..M:

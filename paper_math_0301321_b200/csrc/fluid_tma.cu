@@ -131,7 +131,7 @@ __device__ __forceinline__ void pass_st_flip(const double2 *v, int t, STF st) {
 
 // In-place length-L Stockham transform of the pencil accessed by A(e) (a double2&), by its
 // T threads; every thread of the consumer group must call it (named barrier BAR, NTG).
-template <int L, int SIGN, int C, class ACC, class TW>
+template <int L, int SIGN, int C, bool POW = false, class ACC, class TW>
 __device__ __forceinline__ void fft_inplace(ACC A, int t, TW tw,
                                             int bar, int ntg) {
   double2 v[Plan<L>::RMAX];
@@ -143,13 +143,13 @@ __device__ __forceinline__ void fft_inplace(ACC A, int t, TW tw,
   else pass_st<L, 0>(v, t, st);
   named_bar(bar, ntg);
   if constexpr (Plan<L>::NPASS > 1) {
-    pass_lc<L, SIGN, 1>(v, t, tw, ld);
+    pass_lc<L, SIGN, 1, POW>(v, t, tw, ld);
     named_bar(bar, ntg);
     pass_st<L, 1>(v, t, st);
     named_bar(bar, ntg);
   }
   if constexpr (Plan<L>::NPASS > 2) {
-    pass_lc<L, SIGN, 2>(v, t, tw, ld);
+    pass_lc<L, SIGN, 2, POW>(v, t, tw, ld);
     named_bar(bar, ntg);
     pass_st<L, 2>(v, t, st);
     named_bar(bar, ntg);
@@ -296,7 +296,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
     double2 *pc = buf + comp * K::TILE;
     auto A = [pc, col](int e) -> double2 & { return pc[swz<C>(e, col)]; };
     if (MODE == MODE_Z) {
-      fft_inplace<N, -1, C>(A, t, tw, bar, NTG);
+      fft_inplace<N, -1, C, true>(A, t, tw, bar, NTG);        // z: power twiddles
       if (!IBK_ZHOIST) load_sym();
       const bool ny = (kyg == 0) || (2 * kyg == g.N2g);
       const double lxy = lx + ly;
@@ -329,9 +329,9 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
         solve(kz, q0, q0[0], q0[K::TILE], q0[2 * K::TILE]);
       }
       named_bar(bar, NTG);
-      fft_inplace<N, +1, C>(A, t, tw, bar, NTG);
+      fft_inplace<N, +1, C, true>(A, t, tw, bar, NTG);
     } else {
-      fft_inplace<N, (MODE == MODE_YINV || MODE == MODE_ZINV) ? +1 : -1, C>(A, t, tw, bar, NTG);
+      fft_inplace<N, (MODE == MODE_YINV || MODE == MODE_ZINV) ? +1 : -1, C, ZM>(A, t, tw, bar, NTG);
     }
     fence_proxy_async();                                 // generic writes -> TMA store
     named_bar(bar, NTG);
