@@ -135,6 +135,27 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
   // F is only read on rows the spread touched (row flags), else taken as 0; the flag is
   // loaded before the tile wait so that its latency overlaps the TMA transfer
   const unsigned rflag = (MODE == 0 && rowflag) ? rowflag[(size_t)z * N2 + y] : 1u;
+  // z -+ 1: periodic on the whole lattice; in a slab the neighbours are ghost planes
+  const int zmi = g.slab ? zu - 1 : ((z + N3 - 1) & (N3 - 1));
+  const int zpi = g.slab ? zu + 1 : ((z + 1) & (N3 - 1));
+  const size_t zm = ((size_t)zmi * N2 + y) * N;
+  const size_t zp = ((size_t)zpi * N2 + y) * N;
+  const double *uc_ = u + (MODE == 2 ? 0 : comp * Vu);
+  // the z -+ 1 rows (L2) of the first ZPF pass-0 slots are requested before the tile wait,
+  // so that their latency overlaps the TMA transfer instead of stalling the stencil
+#ifndef IBK_XZPF
+#define IBK_XZPF 2
+#endif
+  constexpr int ZPF = MODE == 2 ? 0 : IBK_XZPF;
+  double2 zpre[ZPF > 0 ? 2 * ZPF : 1];
+  if constexpr (ZPF > 0) {
+    pass0_foreach<M>(t, [&](int slot, int e) {
+      if (slot < ZPF) {
+        zpre[2 * slot] = __ldg(reinterpret_cast<const double2 *>(uc_ + zm + 2 * e));
+        zpre[2 * slot + 1] = __ldg(reinterpret_cast<const double2 *>(uc_ + zp + 2 * e));
+      }
+    });
+  }
   if (MODE != 2 && use_tma) {   // one thread streams the 3 x (RB + 2) rows with TMA
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
@@ -162,18 +183,12 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
     __syncthreads();
   }
   const bool hasF = MODE == 1 || (MODE == 0 && rflag != 0);
-  // z -+ 1: periodic on the whole lattice; in a slab the neighbours are ghost planes
-  const int zmi = g.slab ? zu - 1 : ((z + N3 - 1) & (N3 - 1));
-  const int zpi = g.slab ? zu + 1 : ((z + 1) & (N3 - 1));
-  const size_t zm = ((size_t)zmi * N2 + y) * N;
-  const size_t zp = ((size_t)zpi * N2 + y) * N;
-  const double *uc_ = u + (MODE == 2 ? 0 : comp * Vu);
   const double *own = ut + ((size_t)comp * UR + row + 1) * N;        // this row, own comp
 
   // r at the cell pair (2e, 2e+1) of this thread's component: sum_k u_k D_k^{+-} u_i
   // with the backward difference for u_k > 0 (and u_k = 0, Z5), the forward one for
   // u_k < 0 (PAPER.md 676-691); all operands loaded unconditionally.
-  auto rhs2 = [&](int e) -> double2 {
+  auto rhs2 = [&](int e, int slot) -> double2 {
     const int x = 2 * e;
     const double2 v0 = *reinterpret_cast<const double2 *>(ut + (0 * UR + row + 1) * N + x);
     const double2 v1 = *reinterpret_cast<const double2 *>(ut + (1 * UR + row + 1) * N + x);
@@ -183,8 +198,10 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
     const double xp = own[(x + 2) & (N - 1)];
     const double2 a_ym = *reinterpret_cast<const double2 *>(own - N + x);
     const double2 a_yp = *reinterpret_cast<const double2 *>(own + N + x);
-    const double2 a_zm = __ldg(reinterpret_cast<const double2 *>(uc_ + zm + x));
-    const double2 a_zp = __ldg(reinterpret_cast<const double2 *>(uc_ + zp + x));
+    const double2 a_zm = slot < ZPF ? zpre[2 * slot]
+                                    : __ldg(reinterpret_cast<const double2 *>(uc_ + zm + x));
+    const double2 a_zp = slot < ZPF ? zpre[2 * slot + 1]
+                                    : __ldg(reinterpret_cast<const double2 *>(uc_ + zp + x));
     double2 Fi = make_double2(0.0, 0.0);
     double2 *Fp = reinterpret_cast<double2 *>(F + comp * V + rowbase + x);
     if (hasF) Fi = *Fp;
@@ -202,7 +219,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
 
   double2 rr[Plan<M>::RMAX];
   pass0_foreach<M>(t, [&](int slot, int e) {
-    rr[slot] = MODE == 2 ? __ldg(reinterpret_cast<const double2 *>(in + rowbase) + e) : rhs2(e);
+    rr[slot] = MODE == 2 ? __ldg(reinterpret_cast<const double2 *>(in + rowbase) + e) : rhs2(e, slot);
   });
   if (MODE == 1) {      // r only (debug)
     pass0_foreach<M>(t, [&](int slot, int e) {
