@@ -147,7 +147,7 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
 #define IBK_XZPF 2
 #endif
   constexpr int ZPF = MODE == 2 ? 0 : IBK_XZPF;
-  double2 zpre[ZPF > 0 ? 2 * ZPF : 1];
+  double2 zpre[ZPF > 0 ? 2 * ZPF : 1] = {};
   if constexpr (ZPF > 0) {
     pass0_foreach<M>(t, [&](int slot, int e) {
       if (slot < ZPF) {
