@@ -196,6 +196,23 @@ __device__ __forceinline__ void twiddle16_pow(double2 *v, int e0, TW tw) {
 // POW: radix-16 passes take their twiddles from twiddle16_pow (4 table reads + products)
 // instead of 15 table reads; chosen per kernel by measurement (it frees the latency-bound
 // x forward and z passes, but costs the register-heavy y passes more than it saves).
+// The 15 twiddles of a thread's radix-16 job held in registers for the kernel's lifetime
+// (column passes whose pass-1 job index is the thread's own t, so the set never changes).
+struct RegTw16 {
+  double2 w[16];
+};
+template <class T> struct is_regtw : std::false_type {};
+template <> struct is_regtw<RegTw16> : std::true_type {};
+// w[r] = exp(SIGN 2 pi i e0 r / L) from a device table tw[t] = exp(-2 pi i t / L)
+template <int SIGN>
+__device__ __forceinline__ RegTw16 make_regtw16(const double2 *__restrict__ tw, int e0) {
+  RegTw16 r;
+  r.w[0] = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int k = 1; k < 16; ++k) r.w[k] = twiddle<SIGN>(tw, e0 * k);
+  return r;
+}
+
 template <int L, int SIGN, int PASS, bool POW = false, class TW, class LDF>
 __device__ __forceinline__ void pass_lc(double2 *v, int t, TW tw, LDF ld) {
   using I = PassI<L, PASS>;
@@ -215,7 +232,10 @@ __device__ __forceinline__ void pass_lc(double2 *v, int t, TW tw, LDF ld) {
     const int j = t + q * Plan<L>::T;
     if (I::NS > 1) {
       const int jm = j % I::NS;
-      if constexpr (I::R == 16 && POW) {
+      if constexpr (is_regtw<TW>::value) {
+#pragma unroll
+        for (int r = 1; r < I::R; ++r) v[q * I::R + r] = cmul(v[q * I::R + r], tw.w[r]);
+      } else if constexpr (I::R == 16 && POW) {
         twiddle16_pow<L, SIGN>(&v[q * I::R], jm * (L / (I::NS * I::R)), tw);
       } else {
 #pragma unroll

@@ -199,8 +199,20 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
   __shared__ double2 tws[ZM ? N : 1];
   if constexpr (ZM)
     for (int k = threadIdx.x; k < N; k += blockDim.x) tws[k] = twN[k];
+  // y modes with a 2-pass plan: the pass-1 job of a consumer thread is its own t (J = 1), so
+  // its 15 twiddles are read once into registers (their per-tile table reads were the
+  // largest stall of these passes); z modes read a shared-memory copy with power products
+#ifndef IBK_YREGTW
+#define IBK_YREGTW 1
+#endif
+  constexpr bool YREG = IBK_YREGTW && !ZM && Plan<N>::NPASS == 2 && PassI<N, 1>::J == 1 &&
+                        PassI<N, 1>::R == 16;
+  const int t_cons = (threadIdx.x % K::NTG) / C % K::T;
   const auto tw = [&]() {
     if constexpr (ZM) return SmemTw{tws};
+    else if constexpr (YREG)
+      return make_regtw16<(MODE == MODE_YINV) ? +1 : -1>(
+          twN, (t_cons % PassI<N, 1>::NS) * (N / (PassI<N, 1>::NS * 16)));
     else return twN;
   }();
   if (threadIdx.x == 0) {
