@@ -163,9 +163,15 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
       mbar_expect_tx(&tbar, (uint32_t)(3 * UR * N * 8));
       for (int c = 0; c < 3; ++c) {
         const int rb = (c * uN3 + zu) * N2;
-        tma_load_2d(ut + ((size_t)c * UR + 1) * N, &map_rows, 0, rb + y0, &tbar);
-        tma_load_2d(ut + (size_t)c * UR * N, &map_row1, 0, rb + ((y0 - 1 + N2) & (N2 - 1)), &tbar);
-        tma_load_2d(ut + ((size_t)c * UR + RB + 1) * N, &map_row1, 0, rb + ((y0 + RB) & (N2 - 1)), &tbar);
+        if constexpr (N > 256) {   // rows of 512 doubles: 3-D view (256, 2 halves, row)
+          tma_load_3d(ut + ((size_t)c * UR + 1) * N, &map_rows, 0, 0, rb + y0, &tbar);
+          tma_load_3d(ut + (size_t)c * UR * N, &map_row1, 0, 0, rb + ((y0 - 1 + N2) & (N2 - 1)), &tbar);
+          tma_load_3d(ut + ((size_t)c * UR + RB + 1) * N, &map_row1, 0, 0, rb + ((y0 + RB) & (N2 - 1)), &tbar);
+        } else {
+          tma_load_2d(ut + ((size_t)c * UR + 1) * N, &map_rows, 0, rb + y0, &tbar);
+          tma_load_2d(ut + (size_t)c * UR * N, &map_row1, 0, rb + ((y0 - 1 + N2) & (N2 - 1)), &tbar);
+          tma_load_2d(ut + ((size_t)c * UR + RB + 1) * N, &map_row1, 0, rb + ((y0 + RB) & (N2 - 1)), &tbar);
+        }
       }
     }
     __syncthreads();                                // barrier initialised before anyone waits
@@ -587,7 +593,7 @@ cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, in
 bool xfwd_encode_u(const FluidGeom &g, const double *u, XMapsU *m) {
   m->ok = false;
   const int N = g.N1;
-  if (N > 256 || N < 16) return false;     // box <= 256 doubles; rows >= 128 B (smem alignment)
+  if (N > 512 || N < 16) return false;     // rows >= 128 B (smem alignment)
   void *p = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault,
@@ -599,11 +605,31 @@ bool xfwd_encode_u(const FluidGeom &g, const double *u, XMapsU *m) {
     case 8: rb = XCfg<8>::RB; break;      case 16: rb = XCfg<16>::RB; break;
     case 32: rb = XCfg<32>::RB; break;    case 64: rb = XCfg<64>::RB; break;
     case 128: rb = XCfg<128>::RB; break;  case 256: rb = XCfg<256>::RB; break;
+    case 512: rb = XCfg<512>::RB; break;
     default: return false;
+  }
+  void *base = const_cast<double *>(u);
+#ifndef IBK_X512TMA
+#define IBK_X512TMA 1
+#endif
+  if (N > 256) {          // a TMA box row is at most 256 elements: (256, 2 halves, row) view
+    if (!IBK_X512TMA) return false;
+    cuuint64_t d3[3] = {256, 2, (cuuint64_t)3 * g.N2 * g.uN3};
+    cuuint64_t s3[2] = {256 * 8, (cuuint64_t)N * 8};
+    cuuint32_t b3[3] = {256, 2, (cuuint32_t)rb}, b31[3] = {256, 2, 1}, e3[3] = {1, 1, 1};
+    if (fn(&m->rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, d3, s3, b3, e3,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    if (fn(&m->row1, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, d3, s3, b31, e3,
+           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return false;
+    m->ok = true;
+    return true;
   }
   cuuint64_t dims[2] = {(cuuint64_t)N, (cuuint64_t)3 * g.N2 * g.uN3}, strides[1] = {(cuuint64_t)N * 8};
   cuuint32_t box[2] = {(cuuint32_t)N, (cuuint32_t)rb}, box1[2] = {(cuuint32_t)N, 1u}, es[2] = {1, 1};
-  void *base = const_cast<double *>(u);
   if (fn(&m->rows, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, base, dims, strides, box, es,
          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)

@@ -266,7 +266,7 @@ ib_ctx *ib_create3(int32_t N1, int32_t N2, int32_t N3, double h, double rho, dou
     if ((e = fluid_setup_attributes(L[a])) != cudaSuccess) return bad(e, "attributes");
   if ((e = colfft_make_maps(c->g, c->spec, c->spec2, &c->maps)) != cudaSuccess) return bad(e, "TMA tensor maps");
 #ifndef IBK_NO_XFTMA
-  xfwd_encode_u(c->g, c->u, &c->umaps);   // !ok (cp.async tile copy) when N1 > 256
+  xfwd_encode_u(c->g, c->u, &c->umaps);   // !ok (cp.async tile copy) when N1 < 16
 #endif
 #ifndef IBK_NO_XTMA   // dev switch: the per-CTA row kernels of fluid.cu for comparison
   if (xpass_supported(N1)) {
