@@ -163,9 +163,11 @@ cudaError_t enqueue_step(ib_ctx *c, bool pressure, cudaEvent_t *ev) {
   return launch_step_inc(c->dev_n, s);
 }
 
+// x forward, y forward, z solve, y inverse, x inverse, step counter; force + spread (drive
+// included) and interp with points
 int64_t launches_per_step(const ib_ctx *c, bool pressure) {
   (void)pressure;
-  return 6 + (c->np > 0 ? 2 : 0) + (c->nd > 0 && c->np > 0 ? 1 : 0);
+  return 6 + (c->np > 0 ? 2 : 0);
 }
 
 // One step as a CUDA graph (captured on first use, replayed until invalidated).

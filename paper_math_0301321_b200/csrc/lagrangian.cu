@@ -180,18 +180,14 @@ __global__ void k_drive_add(StructDev sd, const long long *dev_n, long long n, d
   for (int c = 0; c < 3; ++c) f_out[3 * i + c] += a * dir[c];
 }
 
-// Spread of the drive forces (few points): one warp per driven point, each lane owning 2 of
-// the 64 support nodes x 3 components (6 atomics per lane).
-__global__ void k_drive_spread(StructDev sd, FluidGeom g, const long long *dev_n, long long n,
-                               double *F, unsigned *rowflag) {
-  const int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (d >= sd.nd) return;
+// Spread of the drive force of driven point d (few points): one warp per driven point, each
+// lane owning 2 of the 64 support nodes x 3 components (6 atomics per lane).  Run by the
+// first warps of k_force_spread (no launch of its own); a = drive factor / h^3.
+__device__ __forceinline__ void drive_spread_one(const StructDev &sd, const FluidGeom &g, double a,
+                                                 int64_t d, int lane, double *F, unsigned *rowflag) {
   const int N1 = g.N1, N2 = g.N2, N3g = g.N3g;
   const unsigned L = (unsigned)g.N3;           // local planes (all N3 unless a slab)
   const size_t V = (size_t)g.V;
-  const double a = drive_factor(sd, dev_n ? *dev_n : n) * g.invh * g.invh * g.invh;
-  if (a == 0.0) return;
   const int64_t i = sd.drive_idx[d];
   double wx[4], wy[4], wz[4];
   const int jx = axis_weights(sd.X[3 * i + 0], g.invh, wx);
@@ -231,12 +227,12 @@ constexpr int REC = 30;
 constexpr int PTAB = 64;   // patch table entries staged in shared memory
 
 #ifndef IBK_SP_MINB
-#define IBK_SP_MINB 1
+#define IBK_SP_MINB 6   // 80 registers: 6 blocks of 128 per SM (the folded drive pushes it to 94)
 #endif
 template <bool FROM_ARRAY>
 __global__ void __launch_bounds__(SPREAD_THREADS, IBK_SP_MINB)
 k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, double *F,
-               unsigned *rowflag) {
+               unsigned *rowflag, const long long *dev_n, long long n) {
   __shared__ __align__(16) double rec[SPREAD_THREADS / 32][33][REC];   // record 32: zeros (tail)
   __shared__ ib_patch ptab[PTAB];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -246,6 +242,13 @@ k_force_spread(StructDev sd, FluidGeom g, const double *__restrict__ f_in, doubl
   if (lane < REC) rec[warp][32][lane] = 0.0;   // (REC <= 32)
   __syncthreads();
   const ib_patch *pt = small ? ptab : sd.patches;
+  if (!FROM_ARRAY && sd.nd > 0) {             // the drive of this step (few points) first
+    const double a = drive_factor(sd, dev_n ? *dev_n : n) * g.invh * g.invh * g.invh;
+    if (a != 0.0)
+      for (int64_t d = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; d < sd.nd;
+           d += ((int64_t)gridDim.x * blockDim.x) >> 5)
+        drive_spread_one(sd, g, a, d, lane, F, rowflag);
+  }
   const int N1 = g.N1, N2 = g.N2, N3g = g.N3g;
   const unsigned L = (unsigned)g.N3;                     // local planes (all N3 unless a slab)
   const size_t V = (size_t)g.V;
@@ -358,12 +361,10 @@ cudaError_t launch_force_spread(const StructDev &sd, const FluidGeom &g, const d
     const int64_t need = (sd.np + SPREAD_THREADS - 1) / SPREAD_THREADS;
     const unsigned blocks = (unsigned)(need < cap ? need : cap);
     if (f_in)
-      k_force_spread<true><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag);
+      k_force_spread<true><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag, dev_n, n);
     else
-      k_force_spread<false><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag);
+      k_force_spread<false><<<blocks, SPREAD_THREADS, 0, s>>>(sd, g, f_in, F, rowflag, dev_n, n);
   }
-  if (!f_in && sd.nd > 0)
-    k_drive_spread<<<(unsigned)((sd.nd * 32 + 127) / 128), 128, 0, s>>>(sd, g, dev_n, n, F, rowflag);
   return cudaGetLastError();
 }
 

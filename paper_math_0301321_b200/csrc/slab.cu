@@ -189,7 +189,7 @@ int ib_slab_phase(ib_ctx *c, int32_t phase) {
       CK(launch_force_spread(struct_dev(c), g, nullptr, c->dev_n, 0, c->F, c->rowflag, s));
       CK(xfwd(c, 0, c->u, c->F, c->rowflag, nullptr, s));
       CK(yfwd(c, s));
-      c->launches += 2 + (c->np > 0 ? 1 : 0) + (c->nd > 0 && c->np > 0 ? 1 : 0);
+      c->launches += 2 + (c->np > 0 ? 1 : 0);   // the drive runs inside the spread
       return IB_OK;
     }
     case 1:

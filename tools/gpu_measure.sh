@@ -20,8 +20,7 @@ for c in $CFGS; do
       > $OUT/ncu_launch_${TAG}_cfg$c.log 2>&1; echo "ncu launches cfg$c rc=$?"
   # --set full of the last step's kernels (skip create + bin + 2 warm-up steps)
   NL=$(grep -c gpu__time_duration $OUT/launches_${TAG}_cfg$c.csv)
-  PER=9
-  if [ "$c" = "1" ] || [ "$c" = "2" ]; then PER=8; fi
+  PER=8
   SKIP=$(( NL - PER ))
   timeout 1500 ncu --set full --clock-control none --import-source on -s $SKIP -c $PER \
       -o $OUT/prof_${TAG}_cfg$c python tools/prof_step.py --config $c --warmup 2 --steps 1 \

@@ -12,7 +12,8 @@ timeout 900 python bench.py --no-cpu-baseline > $OUT/bench_$TAG.json 2> $OUT/ben
 python -c "
 import json; d=json.load(open('$OUT/bench_$TAG.json'))
 print('steps/s', round(d['value'],1), 'ms', round(d['ms_per_step'],4))
-for k,v in d['stages'].items(): print(f'  {k:16s} {1e3*v[\"ms\"]:8.1f} us  {v[\"gbs\"]:7.0f} GB/s')
+for k,v in d["stages"].items():
+  if "gbs" in v: print(f"  {k:16s} {1e3*v[\"ms\"]:8.1f} us  {v[\"gbs\"]:7.0f} GB/s")
 "
 if [ -n "${NCU_K:-}" ]; then
 python tools/prof_step.py --config 4 --warmup 2 --steps 1 > $OUT/plain_$TAG.log 2>&1 && \

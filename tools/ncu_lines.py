@@ -1,6 +1,8 @@
 """Per-source-line stall samples of one kernel: ncu SASS samples mapped through nvdisasm line info.
 
-  python tools/ncu_lines.py report.ncu-rep <kernel-regex> [skip] [top] [--so path]
+  python tools/ncu_lines.py report.ncu-rep <kernel-regex> [skip] [top] [--so path] [--inst]
+
+--inst ranks lines by executed warp instructions instead of stall samples.
 
 The .so must be the build that was profiled (same sources); the kernel's SASS offsets
 (address - first address) are matched to `nvdisasm -g` line annotations.
@@ -87,7 +89,8 @@ def main():
     tot = 0.0
     for r in data:
         off = int(r[ix["Address"]], 16) - addr0
-        s = float(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+        col = "Instructions Executed" if "--inst" in sys.argv else "Warp Stall Sampling (All Samples)"
+        s = float((r[ix[col]] or "0").replace(",", ""))
         ln = mp.get(off, "?")
         agg[ln] += s
         tot += s
@@ -97,7 +100,7 @@ def main():
                 stall[ln][c[6:]] += float(v)
     for ln, s in agg.most_common(top):
         mix = ", ".join(f"{k} {v:.0f}" for k, v in stall[ln].most_common(3))
-        print(f"{100 * s / max(tot, 1):5.1f}%  {ln:22s} {mix}")
+        print(f"{100 * s / max(tot, 1):5.1f}%  {s:12.0f}  {ln:22s} {mix}")
 
 
 if __name__ == "__main__":

@@ -1,8 +1,8 @@
 """Profiling driver: one warm-up IB step then `--steps` steps of a config (default cfg4).
 
 Used under ncu:  ncu --set full -s <launches to skip> -c <n> python tools/prof_step.py
-Launch order per step: force_spread, drive_spread (if a drive), xfwd, y_fwd, z_solve,
-y_inv, xinv, interp.  ib_create issues 1 launch (tables).
+Launch order per step: force_spread (drive included), xfwd, y_fwd, z_solve,
+y_inv, xinv, interp, step counter.  ib_create issues 1 launch (tables).
 """
 import argparse
 import os
