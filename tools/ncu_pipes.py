@@ -80,7 +80,7 @@ def main():
         mix = ", ".join(f"{c} {100 * v / tot:.0f}%" for c, v in sorted(cls.items(), key=lambda x: -x[1]))
         issue = g(r, "sm__inst_issued.avg.pct_of_peak_sustained_active")
         warps = g(r, "sm__warps_active.avg.pct_of_peak_sustained_active")
-        dram = g(r, "FBSP.TriageCompute.dram__throughput.avg.pct_of_peak_sustained_elapsed")
+        dram = g(r, "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed")
         print(f"   {inst / 1e6:6.1f} M warp instructions ({mix}); issue {issue:4.1f}% of peak, "
               f"warps active {warps:4.1f}%, DRAM {dram:4.1f}% of peak")
         st = [(k2[len("smsp__average_warps_issue_stalled_"):-len("_per_issue_active.ratio")], g(r, k2))
