@@ -142,15 +142,20 @@ __device__ __forceinline__ void fft_inplace(ACC A, int t, TW tw,
   if constexpr (C == 4 && PassI<L, 0>::NS == 1 && Plan<L>::NPASS > 1) pass_st_flip<L, 0>(v, t, st);
   else pass_st<L, 0>(v, t, st);
   named_bar(bar, ntg);
+  // The last pass is thread-local in place (job j reads and writes j + r NS, NS = L / R), so
+  // its stores need no barrier after its loads; the other passes scatter across threads.
+#ifndef IBK_LASTBAR
+#define IBK_LASTBAR 0
+#endif
   if constexpr (Plan<L>::NPASS > 1) {
     pass_lc<L, SIGN, 1, POW>(v, t, tw, ld);
-    named_bar(bar, ntg);
+    if (Plan<L>::NPASS > 2 || IBK_LASTBAR) named_bar(bar, ntg);
     pass_st<L, 1>(v, t, st);
     named_bar(bar, ntg);
   }
   if constexpr (Plan<L>::NPASS > 2) {
     pass_lc<L, SIGN, 2, POW>(v, t, tw, ld);
-    named_bar(bar, ntg);
+    if (IBK_LASTBAR) named_bar(bar, ntg);
     pass_st<L, 2>(v, t, st);
     named_bar(bar, ntg);
   }
