@@ -267,6 +267,38 @@ def test_error_codes(ibm):
         assert e.value.code == ibm.IB_ENONFINITE
 
 
+@pytest.mark.parametrize("N", [16, 64])
+def test_nonfinite_step_reported_as_in_single_steps(ibm, N):
+    """The first non-finite step reported by a multi-step graph run (the step index read on
+    the device) equals the step at which single steps first fail, with the pencil (N = 16)
+    and the TMA (N = 64) x inverse."""
+    import re
+    from gen import Patch, STRETCH1
+    X = np.array([[0.5, 0.5, 0.5], [0.52, 0.5, 0.5]])
+
+    def make(c):
+        c.set_structure(X, [Patch(0, 2, 1, STRETCH1, 0)], np.array([1e30, 0, 1e-6, 0]))
+
+    with ibm.IBContext(N, 1 / N, 1, 0.01, 1e-3) as c:
+        make(c)
+        with pytest.raises(ibm.IBError) as e:
+            c.step(50)
+        assert e.value.code == ibm.IB_ENONFINITE
+        first_graph = int(re.search(r"first at step (\d+)", str(e.value)).group(1))
+    with ibm.IBContext(N, 1 / N, 1, 0.01, 1e-3) as c:
+        make(c)
+        first_single = None
+        for k in range(50):
+            try:
+                c.step(1)
+            except ibm.IBError as e1:
+                assert e1.code == ibm.IB_ENONFINITE
+                first_single = int(re.search(r"first at step (\d+)", str(e1)).group(1))
+                assert first_single == k
+                break
+    assert first_single is not None and first_graph == first_single
+
+
 def test_empty_structure_and_smallest_grid(ibm, olib):
     with ibm.IBContext(8, 1 / 8, 1.0, 0.1, 1e-2) as c:
         c.step(2)
