@@ -129,14 +129,41 @@ __device__ __forceinline__ void pass_st_flip(const double2 *v, int t, STF st) {
   }
 }
 
+#ifndef IBK_LASTBAR
+#define IBK_LASTBAR 0
+#endif
 // In-place length-L Stockham transform of the pencil accessed by A(e) (a double2&), by its
 // T threads; every thread of the consumer group must call it (named barrier BAR, NTG).
-template <int L, int SIGN, int C, bool POW = false, class ACC, class TW>
+// FUSE: at L = 512 fold the radix-2 first pass into the second pass's loads (z modes: the
+// z solve 2240 -> 2080 us at 512^3; the y passes, whose 128-byte-row tiles are read by more
+// threads per pencil element, lost 170-290 us with it)
+template <int L, int SIGN, int C, bool POW = false, bool FUSE = false, class ACC, class TW>
 __device__ __forceinline__ void fft_inplace(ACC A, int t, TW tw,
                                             int bar, int ntg) {
   double2 v[Plan<L>::RMAX];
   auto ld = [&](int e) { return A(e); };
   auto st = [&](int e, double2 x) { A(e) = x; };
+#ifndef IBK_FUSE2
+#define IBK_FUSE2 1
+#endif
+  if constexpr (FUSE && IBK_FUSE2 && Plan<L>::NPASS == 3 && PassI<L, 0>::R == 2) {
+    // L = 512 (radix 2, 16, 16): the radix-2 pass is folded into the loads of the second
+    // pass — its output at e is x[e/2] +- x[e/2 + L/2] (no twiddles at NS = 1) — so the
+    // pencil makes one shared-memory round trip less and two barriers fewer
+    auto ld2 = [&](int e) {
+      const double2 a = A(e >> 1), b = A((e >> 1) + L / 2);
+      return (e & 1) ? csub(a, b) : cadd(a, b);
+    };
+    pass_lc<L, SIGN, 1, POW>(v, t, tw, ld2);
+    named_bar(bar, ntg);
+    pass_st<L, 1>(v, t, st);
+    named_bar(bar, ntg);
+    pass_lc<L, SIGN, 2, POW>(v, t, tw, ld);
+    if (IBK_LASTBAR) named_bar(bar, ntg);
+    pass_st<L, 2>(v, t, st);
+    named_bar(bar, ntg);
+    return;
+  }
   pass_lc<L, SIGN, 0>(v, t, tw, ld);
   named_bar(bar, ntg);
   if constexpr (C == 4 && PassI<L, 0>::NS == 1 && Plan<L>::NPASS > 1) pass_st_flip<L, 0>(v, t, st);
@@ -144,9 +171,6 @@ __device__ __forceinline__ void fft_inplace(ACC A, int t, TW tw,
   named_bar(bar, ntg);
   // The last pass is thread-local in place (job j reads and writes j + r NS, NS = L / R), so
   // its stores need no barrier after its loads; the other passes scatter across threads.
-#ifndef IBK_LASTBAR
-#define IBK_LASTBAR 0
-#endif
   if constexpr (Plan<L>::NPASS > 1) {
     pass_lc<L, SIGN, 1, POW>(v, t, tw, ld);
     if (Plan<L>::NPASS > 2 || IBK_LASTBAR) named_bar(bar, ntg);
@@ -313,7 +337,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
     double2 *pc = buf + comp * K::TILE;
     auto A = [pc, col](int e) -> double2 & { return pc[swz<C>(e, col)]; };
     if (MODE == MODE_Z) {
-      fft_inplace<N, -1, C, true>(A, t, tw, bar, NTG);        // z: power twiddles
+      fft_inplace<N, -1, C, true, true>(A, t, tw, bar, NTG);  // z: power twiddles
       if (!IBK_ZHOIST) load_sym();
       const bool ny = (kyg == 0) || (2 * kyg == g.N2g);
       const double lxy = lx + ly;
@@ -346,9 +370,9 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
         solve(kz, q0, q0[0], q0[K::TILE], q0[2 * K::TILE]);
       }
       named_bar(bar, NTG);
-      fft_inplace<N, +1, C, true>(A, t, tw, bar, NTG);
+      fft_inplace<N, +1, C, true, true>(A, t, tw, bar, NTG);
     } else {
-      fft_inplace<N, (MODE == MODE_YINV || MODE == MODE_ZINV) ? +1 : -1, C, ZM>(A, t, tw, bar, NTG);
+      fft_inplace<N, (MODE == MODE_YINV || MODE == MODE_ZINV) ? +1 : -1, C, ZM, ZM>(A, t, tw, bar, NTG);
     }
     fence_proxy_async();                                 // generic writes -> TMA store
     named_bar(bar, NTG);

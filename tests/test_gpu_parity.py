@@ -607,10 +607,10 @@ def test_spread_interp_degenerate_positions(ibm, olib):
     assert abs(np.sum(F * u) * h ** 3 - np.sum(f * U)) <= 1e-12 * np.sum(np.abs(f * U))
 
 
-@pytest.mark.parametrize("shape", [(64, 64, 512), (128, 64, 512)])
+@pytest.mark.parametrize("shape", [(64, 64, 512), (128, 64, 512), (64, 512, 64)])
 def test_z512_column_passes(ibm, olib, shape):
-    """The 512-long z pencils (2-column tiles, SWIZZLE_32B, 2 consumer groups; the in-place
-    passes' conflict flips, fluid_tma.cu fft_inplace): forward FFT vs numpy, the fluid step
+    """512-long z (and y) pencils: the 3-pass plan whose radix-2 first pass is folded into
+    the second pass's loads (fluid_tma.cu fft_inplace): forward FFT vs numpy, the fluid step
     vs the oracle, and the per-mode solve alone (S3c) vs the oracle's solve."""
     n1, n2, n3 = shape
     rng = np.random.default_rng(81)
