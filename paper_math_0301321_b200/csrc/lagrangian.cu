@@ -503,11 +503,20 @@ k_interp_mma(FluidGeom g, const double *__restrict__ u, double *X, int64_t np, d
       bf[2] = __ldg(u + Vi + e0);     bf[3] = __ldg(u + Vi + e1);
       bf[4] = __ldg(u + 2 * Vi + e0); bf[5] = __ldg(u + 2 * Vi + e1);
       const int nm = __popc(gm);
-      __syncwarp();                                     // previous group's list consumed
-      if ((gm >> lane) & 1u) mlist[warp][__popc(gm & ((1u << lane) - 1u))] = (unsigned char)lane;
-      __syncwarp();
+#ifndef IBK_IRUN
+#define IBK_IRUN 1
+#endif
+      // binned order: a group is almost always a run of consecutive lanes, whose members
+      // are then lo + m without the member list
+      const int glo = __ffs(gm) - 1;
+      const bool run = IBK_IRUN && (gm >> glo) == (nm == 32 ? 0xffffffffu : (1u << nm) - 1u);
+      if (!run) {
+        __syncwarp();                                   // previous group's list consumed
+        if ((gm >> lane) & 1u) mlist[warp][__popc(gm & ((1u << lane) - 1u))] = (unsigned char)lane;
+        __syncwarp();
+      }
       for (int m0 = 0; m0 < nm; m0 += 8) {
-        const int src = m0 + p < nm ? (int)mlist[warp][m0 + p] : -1;
+        const int src = m0 + p < nm ? (run ? glo + m0 + p : (int)mlist[warp][m0 + p]) : -1;
         const double af = src >= 0 ? rec[warp][src][a] : 0.0;
         double d[6][2];
 #pragma unroll
