@@ -416,8 +416,11 @@ def run_slab(args, ws, rank, local):
     with torch.cuda.stream(stream):
         if ws == 1:
             P = args.slab_P
-            run = slabmod.LocalSlabs(cfg, P, stream)
-            par = f"slab{P} emulated on 1 GPU (device copies in place of collectives)"
+            run = slabmod.LocalSlabs(cfg, P, stream, fused=args.slab_fused)
+            par = (f"slab{P} emulated on 1 GPU, fused transposes (peer stores from the y-forward "
+                   f"and z-solve kernels; device copies for the ghost planes and records)"
+                   if args.slab_fused else
+                   f"slab{P} emulated on 1 GPU (device copies in place of collectives)")
         else:
             P = ws
             run = slabmod.DistSlab(cfg)
@@ -442,7 +445,8 @@ def run_slab(args, ws, rank, local):
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": wc, "mode": "slab", "slab_P": P, "clocks": clk.summary(),
+                "config": wc, "mode": "slab", "slab_P": P, "slab_fused": bool(args.slab_fused and ws == 1),
+                "clocks": clk.summary(),
                 "note": "not the headline: --mode replicas (default) is; see DESIGN.md §10"}
         print(json.dumps(line), flush=True)
     return 0
@@ -492,6 +496,8 @@ def main(argv=None):
                     help="replicas (default, the headline): one independent IB run per GPU; "
                          "slab: the z-slab decomposition of one lattice")
     ap.add_argument("--slab-P", type=int, default=4, help="slabs emulated on one GPU (--mode slab, N = 1)")
+    ap.add_argument("--slab-fused", action="store_true",
+                    help="--mode slab, N = 1: fused transposes (ib_slab_set_peers) instead of copies")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-cpu-1thread", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=5)

@@ -174,6 +174,15 @@ int ib_slab_info(ib_ctx *ctx, int32_t *info, int32_t cap);
 int ib_slab_set_buffers(ib_ctx *ctx, void *s2, void *z, double *edge_send, double *edge_recv,
                         void *pack_send, void *pack_recv, uint64_t *count_send,
                         uint64_t *count_recv, int64_t pack_cap);
+/* Fused transposes: with P > 0, s2_peers[d] and z_peers[d] are rank d's s2
+ * and z buffers (device pointers valid in this process: the other contexts of one process,
+ * or peer / IPC-mapped memory of other GPUs), same shapes as this rank's.  Phase 0 then
+ * stores the y-forward blocks bound for rank d straight into z_peers[d][.][rank] and phase 1
+ * the z-solved blocks of source rank d straight into s2_peers[d][.][rank], so the caller
+ * skips the exchanges after phases 0 and 1 and only orders the ranks (every rank's phase 0
+ * before any rank's phase 1, every phase 1 before any phase 2).  P = 0 (arrays may be NULL)
+ * returns to the exchange mode.  P must equal the slab count; after ib_slab_set_buffers. */
+int ib_slab_set_peers(ib_ctx *ctx, int32_t P, void *const *s2_peers, void *const *z_peers);
 /* Enqueue phase 0..4 of the next step (see above); phase 4 advances ib_get_step.  Phases
  * must come in order 0, 1, 2, 3, 4, 0, ... (IB_ESTATE otherwise). */
 int ib_slab_phase(ib_ctx *ctx, int32_t phase);

@@ -189,7 +189,7 @@ template <int N, int MODE>
 __global__ void __launch_bounds__(ColCfg<N, MODE>::K::NTHR, 1)
 k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
          const __grid_constant__ CUtensorMap map_st, double2 *pspec,
-         const double2 *__restrict__ twN, Sym sym) {
+         const double2 *__restrict__ twN, Sym sym, const __grid_constant__ PeerMaps peers) {
   using K = typename ColCfg<N, MODE>::K;
   constexpr int C = K::C, G = K::G, T = K::T, NTG = K::NTG, NT = K::NT, S = K::STAGES;
   constexpr int NC = K::NC, BR = K::BOXR;
@@ -274,6 +274,18 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
       auto store = [&](const Walk &t, int s) {
         const int x = 2 * C * t.x, w = tile_w(t), c0 = NC == 1 ? tile_c(t) : 0;
         const double2 *b = stage0 + (size_t)s * NC * K::TILE;
+        if ((MODE == MODE_YFWD || MODE == MODE_Z) && peers.P) {   // fused slab transposes
+          const int R = peers.rows;
+          for (int c = 0; c < NC; ++c)
+            for (int d = 0; d < peers.P; ++d) {
+              if (MODE == MODE_YFWD)   // ky rows [d Ky, (d+1) Ky) -> rank d's Z [c0][r][.][w]
+                tma_store_4d(&peers.m[d], x, w, 0, c0, b + (c * N + d * R) * C);
+              else                     // kz rows [d L, (d+1) L) -> rank d's S2 [c][r][w][.]
+                tma_store_4d(&peers.m[d], x, 0, w, c, b + c * K::TILE + d * R * C);
+            }
+          bulk_commit();
+          return;
+        }
         for (int c = 0; c < NC; ++c)
           for (int r0 = 0; r0 < N; r0 += BR) {
             const double2 *d = b + c * K::TILE + r0 * C;
@@ -450,6 +462,25 @@ bool colfft_encode_slabz(const FluidGeom &gz, double2 *Z, int P, CUtensorMap *m)
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Peer block view: buffer [comp][P][Ky][L][kx] (pitch gz.P complex), block `blk` of the P
+// axis, as (x, z_l, ky_l, comp) with the P axis folded into the comp stride.
+bool colfft_encode_peer(const FluidGeom &gz, double2 *buf, int P, int blk, int C, int zbox,
+                        int kybox, CUtensorMap *m) {
+  auto fn = encode_fn();
+  const int L = gz.L, Ky = gz.N2;
+  if (!fn || P < 1 || P > MAX_PEERS || blk < 0 || blk >= P) return false;
+  const cuuint64_t row = (cuuint64_t)gz.P * 16;
+  cuuint64_t dims[4] = {(cuuint64_t)2 * (gz.M + 1), (cuuint64_t)L, (cuuint64_t)Ky, 3};
+  cuuint64_t strides[3] = {row, row * L, row * L * Ky * P};
+  cuuint32_t box[4] = {(cuuint32_t)(2 * C), (cuuint32_t)zbox, (cuuint32_t)kybox, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  double2 *base = buf + (size_t)blk * Ky * L * gz.P;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, base, dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE,
+            C == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool colfft_supported(int N) { return N >= 64 && N <= 512; }
 
 bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m) {
@@ -483,7 +514,7 @@ static int one_per_sm_grid(Kern k, int threads, size_t smem, int ntiles) {
 template <int N, int MODE>
 static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
                                    const CUtensorMap &st, double2 *pspec, const double2 *twN,
-                                   const Sym &sym, cudaStream_t s) {
+                                   const Sym &sym, cudaStream_t s, const PeerMaps &peers) {
   using K = typename ColCfg<N, MODE>::K;
   static PerDeviceOnce attr;
   const int dev = current_device();
@@ -496,7 +527,7 @@ static cudaError_t launch_colfft_n(const FluidGeom &g, const CUtensorMap &ld,
   constexpr bool YM = MODE == MODE_YFWD || MODE == MODE_YINV;
   const int NB = (g.M + 1 + K::C - 1) / K::C, W = YM ? g.N3 : g.N2;   // tiles per w, w range
   const int grid = one_per_sm_grid(k_colfft<N, MODE>, K::NTHR, K::SMEM, NB * W * (K::NC == 1 ? 3 : 1));
-  k_colfft<N, MODE><<<grid, K::NTHR, K::SMEM, s>>>(g, ld, st, pspec, twN, sym);
+  k_colfft<N, MODE><<<grid, K::NTHR, K::SMEM, s>>>(g, ld, st, pspec, twN, sym, peers);
   return cudaGetLastError();
 }
 
@@ -504,11 +535,12 @@ template <int N>
 static cudaError_t colfft_n(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,
                             const double2 *twN, const Sym &sym, cudaStream_t s) {
   if constexpr (N >= 64 && N <= 512) {
-    if (mode == MODE_ZINV) return launch_colfft_n<N, MODE_ZINV>(g, m.s2_2d, m.s2_2d, nullptr, twN, sym, s);
-    if (mode == MODE_ZFWD) return launch_colfft_n<N, MODE_ZFWD>(g, m.s2_2d, m.s2_2d, nullptr, twN, sym, s);
-    if (mode == MODE_Z) return launch_colfft_n<N, MODE_Z>(g, m.s2_2d, m.s2_2d, pspec, twN, sym, s);
-    if (mode == MODE_YFWD) return launch_colfft_n<N, MODE_YFWD>(g, m.s1_2d, m.s2_3d, nullptr, twN, sym, s);
-    return launch_colfft_n<N, MODE_YINV>(g, m.s2_3d, m.s1_2d, nullptr, twN, sym, s);
+    const PeerMaps none{};
+    if (mode == MODE_ZINV) return launch_colfft_n<N, MODE_ZINV>(g, m.s2_2d, m.s2_2d, nullptr, twN, sym, s, none);
+    if (mode == MODE_ZFWD) return launch_colfft_n<N, MODE_ZFWD>(g, m.s2_2d, m.s2_2d, nullptr, twN, sym, s, none);
+    if (mode == MODE_Z) return launch_colfft_n<N, MODE_Z>(g, m.s2_2d, m.s2_2d, pspec, twN, sym, s, m.peers);
+    if (mode == MODE_YFWD) return launch_colfft_n<N, MODE_YFWD>(g, m.s1_2d, m.s2_3d, nullptr, twN, sym, s, m.peers);
+    return launch_colfft_n<N, MODE_YINV>(g, m.s2_3d, m.s1_2d, nullptr, twN, sym, s, none);
   }
   return cudaErrorInvalidValue;
 }

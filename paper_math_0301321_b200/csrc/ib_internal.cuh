@@ -59,9 +59,21 @@ struct Sym {
 };
 
 // TMA descriptors of the two spectrum arrays (fluid_tma.cu), valid when ok.
+// Slab decomposition with fused transposes: the y forward pass stores the Ky
+// rows of its tiles bound for rank d straight into rank d's receive buffer Z (map m[d]), the
+// z pass the L rows of each source rank straight back into that rank's S2 — peer stores in
+// place of the two all-to-alls.  P = 0: exchange mode (local stores, caller's collectives).
+constexpr int MAX_PEERS = 8;
+struct PeerMaps {
+  CUtensorMap m[MAX_PEERS];
+  int P = 0;
+  int rows = 0;          // rows of one destination block in the tile (y: Ky, z: L)
+};
+
 struct TmaMaps {
   CUtensorMap s1_2d, s2_2d, s2_3d;
   bool y_ok = false, z_ok = false;   // y passes (s1_2d, s2_3d) / z passes (s2_2d) available
+  PeerMaps peers;                    // fused slab transposes (y forward / z solve), or P = 0
 };
 
 // TMA descriptors of the forward x pass (fluid.cu): u rows, RB-row and 1-row boxes.
@@ -200,6 +212,10 @@ cudaError_t launch_xinv(const FluidGeom &g, const double2 *spec, double *out, in
 bool colfft_supported(int N);
 bool colfft_encode_s2(const FluidGeom &g, double2 *base, CUtensorMap *m);
 bool colfft_encode_slabz(const FluidGeom &gz, double2 *Z, int P, CUtensorMap *m);
+// 4-D view (x, z_l, ky_l, comp) of one [comp][P][Ky][L] block column of a peer's S2 or Z
+// buffer starting at block `blk`; box {2C, zbox, kybox, 1}
+bool colfft_encode_peer(const FluidGeom &gz, double2 *buf, int P, int blk, int C, int zbox,
+                        int kybox, CUtensorMap *m);
 cudaError_t colfft_make_maps(const FluidGeom &g, double2 *spec, double2 *spec2, TmaMaps *m);
 // twN: twiddles of the pencil axis (y for modes 1-2, z for 0, 3, 4)
 cudaError_t launch_colfft(const FluidGeom &g, int mode, const TmaMaps &m, double2 *pspec,

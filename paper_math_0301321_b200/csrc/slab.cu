@@ -169,6 +169,37 @@ int ib_slab_set_buffers(ib_ctx *c, void *s2, void *z, double *edge_send, double 
   return IB_OK;
 }
 
+int ib_slab_set_peers(ib_ctx *c, int32_t P, void *const *s2_peers, void *const *z_peers) {
+  if (!c) return fail(IB_EINVAL, "ctx is NULL");
+  if (!c->slab_P) return fail(IB_ESTATE, "not a slab context");
+  if (!c->z_ext) return fail(IB_ESTATE, "ib_slab_set_buffers first");
+  CK(cudaStreamSynchronize(c->stream));
+  if (P == 0) {
+    c->maps.peers.P = 0;
+    c->zmaps.peers.P = 0;
+    return IB_OK;
+  }
+  if (P != c->slab_P) return fail(IB_EINVAL, "P must equal the slab count");
+  if (P > MAX_PEERS) return fail(IB_EINVAL, "at most " + std::to_string(MAX_PEERS) + " peers");
+  if (!s2_peers || !z_peers) return fail(IB_EINVAL, "NULL peer array");
+  for (int d = 0; d < P; ++d)
+    if (!s2_peers[d] || !z_peers[d]) return fail(IB_EINVAL, "NULL peer buffer");
+  const int L = c->g.L, Ky = c->gz.N2, r = c->slab_rank;
+  const int cy = 8, cz = c->gz.N3 >= 128 ? 4 : 8;   // the y / z tiles' columns (fluid_tma.cu)
+  PeerMaps y{}, z{};
+  for (int d = 0; d < P; ++d) {
+    if (!colfft_encode_peer(c->gz, static_cast<double2 *>(z_peers[d]), P, r, cy, 1, Ky, &y.m[d]) ||
+        !colfft_encode_peer(c->gz, static_cast<double2 *>(s2_peers[d]), P, r, cz, L, 1, &z.m[d]))
+      return fail(IB_EINVAL, "peer TMA maps");
+  }
+  y.P = z.P = P;
+  y.rows = Ky;
+  z.rows = L;
+  c->maps.peers = y;
+  c->zmaps.peers = z;
+  return IB_OK;
+}
+
 int ib_slab_phase(ib_ctx *c, int32_t phase) {
   if (!c) return fail(IB_EINVAL, "ctx is NULL");
   if (!c->slab_P) return fail(IB_ESTATE, "not a slab context");

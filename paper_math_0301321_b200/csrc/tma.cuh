@@ -81,6 +81,13 @@ __device__ __forceinline__ void tma_store_5d(const CUtensorMap *m, int c0, int c
       ::"l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(src))
       : "memory");
 }
+__device__ __forceinline__ void tma_store_4d(const CUtensorMap *m, int c0, int c1, int c2, int c3,
+                                             const void *src) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.global.shared::cta.tile.bulk_group [%0, {%1, %2, %3, %4}], [%5];\n"
+      ::"l"(m), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(src))
+      : "memory");
+}
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap *m, int x, int y, const void *src) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n"
                ::"l"(m), "r"(x), "r"(y), "r"(smem_u32(src))

@@ -24,7 +24,7 @@ EXPORTS = ("ib_create", "ib_create3", "ib_destroy", "ib_set_stream", "ib_set_opt
            "ib_get_positions", "ib_rebin", "ib_get_step", "ib_set_step", "ib_num_points", "ib_stage_times",
            "ib_launch_count", "ib_last_error", "ib_debug_force", "ib_debug_spread",
            "ib_debug_interp", "ib_debug_rhs", "ib_debug_fluid", "ib_debug_project",
-           "ib_debug_fft", "ib_debug_ifft", "ib_slab_create", "ib_slab_info", "ib_slab_set_buffers",
+           "ib_debug_fft", "ib_debug_ifft", "ib_slab_create", "ib_slab_info", "ib_slab_set_buffers", "ib_slab_set_peers",
            "ib_slab_phase", "ib_slab_sync")
 
 
@@ -94,6 +94,7 @@ def load(path: Optional[str] = None):
     L.ib_slab_create.argtypes = [i32, i32, i32, d, d, d, d, i32, i32]
     L.ib_slab_info.argtypes = [p, p, i32]
     L.ib_slab_set_buffers.argtypes = [p, p, p, p, p, p, p, p, p, i64]
+    L.ib_slab_set_peers.argtypes = [p, i32, p, p]
     L.ib_slab_phase.argtypes = [p, i32]
     L.ib_slab_sync.argtypes = [p]
     for name in EXPORTS:

@@ -158,10 +158,24 @@ def exchange_dist(rank, phase: int, group=None) -> None:
 
 
 # ------------------------------------------------------------------ drivers
-class LocalSlabs:
-    """P slab ranks of one lattice in one process on the current GPU, all on one stream."""
+def set_peers(rank, s2_ptrs: Sequence[int], z_ptrs: Sequence[int]) -> None:
+    """Fused transposes for `rank` (ib_slab_set_peers): phase 0 / 1 store straight into the
+    peers' z / s2 buffers (device pointers valid in this process); empty lists switch back
+    to the exchange mode."""
+    P = len(s2_ptrs)
+    arr = C.c_void_p * max(P, 1)
+    _check(load().ib_slab_set_peers(rank.ctx, P, arr(*s2_ptrs) if P else None,
+                                    arr(*z_ptrs) if P else None))
 
-    def __init__(self, cfg, P: int, stream=None):
+
+class LocalSlabs:
+    """P slab ranks of one lattice in one process on the current GPU, all on one stream.
+
+    fused=True: the y-forward and z-solve kernels store the transposed blocks straight into
+    the other ranks' buffers (ib_slab_set_peers) — no copies after phases 0 and 1; the one
+    stream orders the ranks' phases."""
+
+    def __init__(self, cfg, P: int, stream=None, fused: bool = False):
         import torch
         self.cfg = cfg
         self.P = int(P)
@@ -172,6 +186,15 @@ class LocalSlabs:
         assert self.stream.cuda_stream != 0, "LocalSlabs needs a non-default stream"
         for r in self.ranks:
             r.set_stream(self.stream.cuda_stream)
+        self.set_fused(fused)
+
+    def set_fused(self, fused: bool):
+        """Switch between fused transposes (peer stores) and the exchange copies."""
+        self.fused = bool(fused)
+        s2 = [q.s2.data_ptr() for q in self.ranks] if self.fused else []
+        z = [q.z.data_ptr() for q in self.ranks] if self.fused else []
+        for r in self.ranks:
+            set_peers(r, s2, z)
 
     def step(self, nsteps: int = 1):
         import torch
@@ -180,7 +203,7 @@ class LocalSlabs:
                 for ph in range(5):
                     for r in self.ranks:
                         r.phase(ph)
-                    if ph < 4:
+                    if ph < 4 and not (self.fused and ph < 2):
                         exchange_local(self.ranks, ph)
         for r in self.ranks:
             r.sync()
@@ -210,10 +233,29 @@ class LocalSlabs:
         self.close()
 
 
-class DistSlab:
-    """This process's rank of a P-GPU slab decomposition (torch.distributed, NCCL)."""
+def _peer_views(t, group):
+    """Every rank's copy of buffer t as a tensor mapped into this process: CUDA IPC handles
+    (torch's tensor sharing) exchanged with all_gather_object; this rank's own entry is t."""
+    import torch.distributed as dist
+    from torch.multiprocessing.reductions import reduce_tensor
+    P, me = dist.get_world_size(group), dist.get_rank(group)
+    if P == 1:
+        return [t]
+    shared = [None] * P
+    dist.all_gather_object(shared, reduce_tensor(t), group=group)
+    return [t if d == me else shared[d][0](*shared[d][1]) for d in range(P)]
 
-    def __init__(self, cfg, group=None):
+
+class DistSlab:
+    """This process's rank of a P-GPU slab decomposition (torch.distributed, NCCL).
+
+    fused=True: the y-forward and z-solve kernels store the transposed blocks straight into
+    the peers' buffers (mapped with CUDA IPC; NVLink peer stores), and a one-element NCCL
+    all-reduce on the phase stream orders the ranks after phases 0 and 1 instead of the two
+    all-to-alls.  Only a world of one rank (peers = itself) is exercised on this pool's
+    one-GPU boxes; the IPC mapping across GPUs is untested here."""
+
+    def __init__(self, cfg, group=None, fused: bool = False):
         import torch
         import torch.distributed as dist
         self.group = group
@@ -221,15 +263,25 @@ class DistSlab:
         self.rank = SlabRank.from_config(cfg, P, rank)
         self.stream = torch.cuda.Stream()          # non-default: see LocalSlabs
         self.rank.set_stream(self.stream.cuda_stream)
+        self.fused = bool(fused)
+        if self.fused:
+            self._s2 = _peer_views(self.rank.s2, group)      # keep the mappings alive
+            self._z = _peer_views(self.rank.z, group)
+            set_peers(self.rank, [t.data_ptr() for t in self._s2], [t.data_ptr() for t in self._z])
+            self._tick = torch.zeros(1, dtype=torch.float64, device=self.rank.s2.device)
 
     def step(self, nsteps: int = 1):
         import torch
+        import torch.distributed as dist
         with torch.cuda.stream(self.stream):      # the collectives wait on this stream
             for _ in range(int(nsteps)):
                 for ph in range(5):
                     self.rank.phase(ph)
                     if ph < 4:
-                        exchange_dist(self.rank, ph, self.group)
+                        if self.fused and ph < 2:  # peer stores landed on every rank
+                            dist.all_reduce(self._tick, group=self.group)
+                        else:
+                            exchange_dist(self.rank, ph, self.group)
         self.rank.sync()
 
     def close(self):

@@ -157,6 +157,41 @@ def test_slab_replicas_agree_and_match_the_whole_lattice(slabm):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("P", [2, 4, 8])
+def test_fused_slab_small_sheet_matches_oracle(slabm, olib, P):
+    """Fused transposes (ib_slab_set_peers): the y-forward and z-solve kernels store the
+    transposed blocks straight into the other ranks' buffers, no exchange after phases 0-1."""
+    cfg = small_sheet_config(N=64, n1=40, n2=30, seed=61, u_amp=0.2, dt=2.5e-4)
+    print(step_parity(olib, cfg, lambda: slabm.LocalSlabs(cfg, P, fused=True), check_U=False))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("shape,P", [((64, 128, 64), 4), ((128, 64, 256), 2), ((64, 64, 512), 8)])
+def test_fused_slab_equals_exchange_slab(slabm, shape, P):
+    """The fused step against the exchange step on anisotropic lattices (z tiles of 8 and 4
+    columns, L from 8 to 256): u and X agree to fp64 summation order (spread atomics)."""
+    cfg = small_sheet_config(N=shape, n1=30, n2=24, seed=63, u_amp=0.3, dt=2.5e-4)
+    with slabm.LocalSlabs(cfg, P) as a, slabm.LocalSlabs(cfg, P, fused=True) as b:
+        a.step(4)
+        b.step(4)
+        ua, _ = a.get_fields()
+        ub, _ = b.get_fields()
+        assert rel_l2(ub, ua) < 1e-13
+        assert rel_l2(b.get_positions() - cfg.X, a.get_positions() - cfg.X) < 1e-11
+        b.set_fused(False)                          # back to the exchange mode
+        b.step(2)
+        a.step(2)
+        assert rel_l2(b.get_fields()[0], a.get_fields()[0]) < 1e-13
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_fused_slab_config4_matches_oracle(slabm, olib):
+    print(step_parity(olib, make_config(4), lambda: slabm.LocalSlabs(make_config(4), 4, fused=True),
+                      check_U=False))
+
+
+@pytest.mark.gpu
 def test_slab_rejects_bad_decompositions(slabm):
     from paper_math_0301321_b200.ib import IBError
     for N, P in (((64, 64, 64), 16), ((64, 64, 64), 3), ((32, 64, 64), 2)):
@@ -165,7 +200,8 @@ def test_slab_rejects_bad_decompositions(slabm):
 
 
 @pytest.mark.gpu
-def test_distslab_nccl_world1_matches_oracle(slabm, olib):
+@pytest.mark.parametrize("fused", [False, True])
+def test_distslab_nccl_world1_matches_oracle(slabm, olib, fused):
     """The torch.distributed path (DistSlab: NCCL all_to_all_single / all_gather_into_tensor
     between the phases) in a world of one rank on the box's one GPU, against the oracle at
     steps 1, 2, 10.  (Several ranks need several GPUs; the exchange layout for P = 2 is
@@ -179,7 +215,7 @@ def test_distslab_nccl_world1_matches_oracle(slabm, olib):
 
         class _Run:
             def __init__(self):
-                self.d = slabm.DistSlab(cfg)
+                self.d = slabm.DistSlab(cfg, fused=fused)
 
             def step(self, k):
                 self.d.step(k)
