@@ -17,6 +17,10 @@
 //      the owned points (base plane in the slab), packed as (x, y, z, index) records
 //        [caller: all-gather count_send -> count_recv, pack_send -> pack_recv]
 //   4  every rank's records scattered into this rank's replica of X; step counter + 1
+// With ib_slab_set_peers the two transposes are fused into the kernels: phase 0's y-forward
+// pass stores each tile's Ky-row block bound for rank d straight into rank d's Z, phase 1's
+// z solve each L-row block of source rank d straight into rank d's S2 (TMA stores through
+// per-peer maps), and the caller only orders the ranks after phases 0 and 1.
 // Positions are replicated on every rank; each rank computes the forces of the points whose
 // support meets its planes and spreads only onto its own planes, so the spread needs no
 // halo reduction.

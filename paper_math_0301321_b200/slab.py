@@ -10,6 +10,9 @@ them between the phases:
   after phase 2   all-gather of the edge planes (ghost planes of u)
   after phase 3   all-gather of the owned points' X^{n+1} records (replicated X)
 
+With fused=True the first two exchanges disappear: the y-forward and z-solve kernels store
+the transposed blocks straight into the peers' s2 / z buffers (ib_slab_set_peers).
+
 `LocalSlabs` runs P slab contexts in one process on one GPU with device copies in place of
 the collectives (the parity harness: the decomposition is checked against the oracle on a
 single GPU); `DistSlab` is one rank of a torch.distributed job (NCCL across GPUs) using the
