@@ -15,10 +15,5 @@ fi
 tail -40 $OUT/pytest_gpu_$TAG.log | grep -v "^$" | tail -32
 if [ "${NO_BENCH:-0}" != "1" ]; then
 timeout 900 python bench.py --no-cpu-baseline > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"
-python -c "
-import json; d=json.load(open('$OUT/bench_$TAG.json'))
-print('steps/s', round(d['value'],1), 'ms', round(d['ms_per_step'],4))
-for k,v in d["stages"].items():
-  if "gbs" in v: print(f"  {k:16s} {1e3*v[\"ms\"]:8.1f} us  {v[\"gbs\"]:7.0f} GB/s")
-"
+python tools/bench_summary.py $OUT/bench_$TAG.json
 fi

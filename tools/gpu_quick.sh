@@ -9,12 +9,7 @@ python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $OUT/smoke_$TAG.
 timeout 1200 python -m pytest tests -m gpu -x -q > $OUT/pytest_gpu_$TAG.log 2>&1; echo "pytest rc=$?"
 tail -3 $OUT/pytest_gpu_$TAG.log
 timeout 900 python bench.py --no-cpu-baseline > $OUT/bench_$TAG.json 2> $OUT/bench_$TAG.err; echo "bench rc=$?"
-python -c "
-import json; d=json.load(open('$OUT/bench_$TAG.json'))
-print('steps/s', round(d['value'],1), 'ms', round(d['ms_per_step'],4))
-for k,v in d["stages"].items():
-  if "gbs" in v: print(f"  {k:16s} {1e3*v[\"ms\"]:8.1f} us  {v[\"gbs\"]:7.0f} GB/s")
-"
+python tools/bench_summary.py $OUT/bench_$TAG.json
 if [ -n "${NCU_K:-}" ]; then
 python tools/prof_step.py --config 4 --warmup 2 --steps 1 > $OUT/plain_$TAG.log 2>&1 && \
 ncu --set full --clock-control none --import-source on -k "regex:${NCU_K}" -s ${NCU_S:-0} -c ${NCU_C:-4} \
