@@ -11,6 +11,7 @@ timeout 2400 python -m pytest tests -m gpu -q -s --durations=15 > gpurun_out/pyt
 EXPER=${EXPER:-1} bash tools/gpu_measure.sh $TAG "4 1 2 3 5 4h"
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
 timeout 600 python bench.py --mode slab --slab-P 4 --steps 20 --warmup 3 > gpurun_out/bench_slab_$TAG.json 2> gpurun_out/bench_slab_$TAG.err; echo "slab rc=$?"
+timeout 600 python bench.py --mode slab --slab-P 4 --slab-fused --steps 20 --warmup 3 > gpurun_out/bench_slabf_$TAG.json 2> gpurun_out/bench_slabf_$TAG.err; echo "slab fused rc=$?"
 # launch list of the bench command itself (cold-cache, serialised: compare shares, not times)
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 200 --csv \
     --log-file gpurun_out/launches_${TAG}b.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline \
