@@ -367,7 +367,7 @@ k_colfft(FluidGeom g, const __grid_constant__ CUtensorMap map_ld,
         } else {
           // one division: w = 1/(d |s|^2) gives 1/d = w |s|^2 and 1/|s|^2 = w d
           const double s2 = sx * sx + sy * sy + sz * sz;
-          const double w = 1.0 / (d * s2);
+          const double w = rcp_pos(d * s2);
           const double is2 = w * d, inv = invV * (w * s2);
           const double2 q = make_double2((sx * r0.x + sy * r1.x + sz * r2.x) * is2,
                                          (sx * r0.y + sy * r1.y + sz * r2.y) * is2);
