@@ -156,6 +156,32 @@ k_xfwd(FluidGeom g, const double *__restrict__ u, double *F, unsigned *rowflag,
       }
     });
   }
+  // N1 = 512: the z -+ 1 rows of the remaining slots are prefetched into L1 (no registers),
+  // also before the tile wait: x forward 2244 -> 2093 us at 512^3 (6 slots: 2192); at
+  // N1 = 256 the same prefetch is neutral to slower (243.7 -> 245.9 us, 6 slots 250), so off
+#ifndef IBK_XL1PF
+#define IBK_XL1PF (N >= 512 ? 16 : 0)
+#endif
+  constexpr int L1PF = IBK_XL1PF;
+  if constexpr (MODE != 2 && L1PF > 0) {
+    pass0_foreach<M>(t, [&](int slot, int e) {
+      if (slot >= ZPF && slot < ZPF + L1PF) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(uc_ + zm + 2 * e));
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(uc_ + zp + 2 * e));
+      }
+    });
+  }
+  // the F of a flagged row is prefetched into L1 likewise (x forward 2089 -> 2039 us at 512^3,
+  // 243.7 -> 242.2 us at 256^3)
+#ifndef IBK_XFPF
+#define IBK_XFPF 1
+#endif
+  if constexpr (MODE == 0 && IBK_XFPF) {
+    if (rflag != 0)
+      pass0_foreach<M>(t, [&](int slot, int e) {
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(F + comp * V + rowbase + 2 * e));
+      });
+  }
   if (MODE != 2 && use_tma) {   // one thread streams the 3 x (RB + 2) rows with TMA
     if (threadIdx.x == 0) {
       mbar_init(&tbar, 1);
