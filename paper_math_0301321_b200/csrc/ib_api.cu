@@ -61,7 +61,9 @@ StructDev struct_dev(const ib_ctx *c) {
 
 void free_graph(ib_ctx *c) {
   if (c->graph) cudaGraphExecDestroy(c->graph);
+  if (c->graph_chunk) cudaGraphExecDestroy(c->graph_chunk);
   c->graph = nullptr;
+  c->graph_chunk = nullptr;
   c->graph_key = -1;
 }
 
@@ -170,20 +172,23 @@ int64_t launches_per_step(const ib_ctx *c, bool pressure) {
   return 6 + (c->np > 0 ? 2 : 0);
 }
 
-// One step as a CUDA graph (captured on first use, replayed until invalidated).
-cudaError_t graph_step(ib_ctx *c) {
-  if (!c->graph) {
+// m = 1 or GRAPH_CHUNK consecutive steps as a CUDA graph (captured on first use, replayed
+// until invalidated).  The chunk graph saves the graph-to-graph launch gap of the steps
+// inside it; ib_step uses it when no re-binning falls inside the chunk.
+cudaError_t graph_steps(ib_ctx *c, int m) {
+  cudaGraphExec_t &ge = m == 1 ? c->graph : c->graph_chunk;
+  if (!ge) {
     cudaGraph_t gr = nullptr;
     cudaError_t e = cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) return e;
-    e = enqueue_step(c, false, nullptr);
+    for (int k = 0; k < m && e == cudaSuccess; ++k) e = enqueue_step(c, false, nullptr);
     cudaError_t e2 = cudaStreamEndCapture(c->stream, &gr);
     if (e == cudaSuccess) e = e2;
-    if (e == cudaSuccess) e = cudaGraphInstantiate(&c->graph, gr, 0);
+    if (e == cudaSuccess) e = cudaGraphInstantiate(&ge, gr, 0);
     if (gr) cudaGraphDestroy(gr);
-    if (e != cudaSuccess) { c->graph = nullptr; return e; }
+    if (e != cudaSuccess) { ge = nullptr; return e; }
   }
-  return cudaGraphLaunch(c->graph, c->stream);
+  return cudaGraphLaunch(ge, c->stream);
 }
 
 struct Tmp {
@@ -529,16 +534,23 @@ int ib_step(ib_ctx *c, int32_t nsteps) {
   const long long n0 = c->n;
   CK(cudaMemcpyAsync(c->dev_n, &n0, sizeof(long long), cudaMemcpyHostToDevice, s));
   CK(cudaStreamSynchronize(s));                 // n0 lives on the host stack
-  for (int32_t k = 0; k < nsteps; ++k) {
+  for (int32_t k = 0; k < nsteps;) {
     const bool pressure = c->want_p && k == nsteps - 1;
     CK(ensure_binned(c, s));                    // outside the graph (it holds only pointers)
+    int32_t m = 1;
     if (c->use_graph && !timing && !pressure) {
-      CK(graph_step(c));
+      // GRAPH_CHUNK steps in one graph when neither the next re-binning (same schedule as
+      // step by step: every SORT_PERIOD steps) nor the pressure step falls inside them
+      const int32_t plain_left = nsteps - k - (c->want_p ? 1 : 0);
+      const bool room = c->np == 0 || c->since_bin + GRAPH_CHUNK <= SORT_PERIOD;
+      if (plain_left >= GRAPH_CHUNK && room) m = GRAPH_CHUNK;
+      CK(graph_steps(c, m));
     } else {
       CK(enqueue_step(c, pressure, timing ? &c->ev_pool[k * per] : nullptr));
     }
-    c->since_bin++;
-    c->launches += launches_per_step(c, pressure);
+    c->since_bin += m;
+    c->launches += m * launches_per_step(c, pressure);
+    k += m;
   }
   CK(cudaMemcpyAsync(c->flag_h, c->flag, sizeof(long long), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));

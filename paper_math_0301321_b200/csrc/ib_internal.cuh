@@ -163,7 +163,8 @@ struct ib_ctx {
   std::vector<cudaEvent_t> ev_pool;   // per-step stage events (IB_OPT_STAGE_TIMING)
   int64_t launches = 0;
   // CUDA graph of one step (rebuilt after any change of structure, drive, stream, options)
-  cudaGraphExec_t graph = nullptr;
+  cudaGraphExec_t graph = nullptr;        // one step
+  cudaGraphExec_t graph_chunk = nullptr;  // GRAPH_CHUNK steps
   long long graph_key = -1;
   long long *dev_n = nullptr;   // device step counter (drive phase, non-finite flag)
   // slab decomposition along z (ib_slab_create): rank slab_rank of slab_P.
@@ -272,5 +273,12 @@ cudaError_t launch_gather_xs(const double *X, const int *perm, int64_t np, doubl
                              cudaStream_t s);
 int bin_scan_blocks(int64_t V);
 cudaError_t launch_step_inc(long long *dev_n, cudaStream_t s);
+// measured on one pod, ms/step with chunks of 1 / 4 / 8 / 32 steps: cfg1 0.0509 / 0.0496 /
+// 0.0516 / 0.0512, cfg2 0.0623 / 0.0606 / 0.0627 / 0.0617, cfg3 0.1559 / 0.1539 / 0.1559 /
+// 0.1539, cfg4 1.148 / 1.148 / 1.151 / 1.149
+#ifndef IBK_GRAPH_CHUNK
+#define IBK_GRAPH_CHUNK 4
+#endif
+constexpr int GRAPH_CHUNK = IBK_GRAPH_CHUNK;    // steps per chunk graph (divides SORT_PERIOD)
 constexpr int SORT_PERIOD = 32;   // steps between re-binnings inside ib_step
 }  // namespace ibk
